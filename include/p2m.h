@@ -123,8 +123,9 @@ int p2m_nearest_site_device(p2m_engine *engine, int slot, const double *d_q_xyz,
 int p2m_query_device_counters(p2m_engine *engine, int slot, const double *d_q_xyz, uint64_t n,
                               uint64_t *d_per_query, void *stream);
 
-/* Kernel-split timing of one p2m_query_device call (ms, CUDA events on the call's stream):
- * [0] morton keys, [1] sort, [2] fused query, total in [3].  Enabled by p2m_set_profiling. */
+/* Kernel-split timing (ms, CUDA events recorded on each call's own stream, no host sync):
+ * [0] morton keys, [1] sort, [2] fused query, [3] total -- mean over the p2m_query_device calls
+ * recorded since p2m_set_profiling(e, 1) (up to 256), then the record is reset. */
 int p2m_set_profiling(p2m_engine *engine, int enable);
 int p2m_last_timings(p2m_engine *engine, int slot, float *ms4);
 

@@ -1,0 +1,602 @@
+// p2m_engine.cu -- the device engine behind the C ABI (include/p2m.h): packs the built structure
+// into the device layout, uploads it to the first GPU, replicates it to the others by a one-time
+// peer copy, and runs the query pipeline (Morton keys -> CUB radix sort -> fused query kernel).
+//
+// Multi-GPU: queries are independent (REF/SPEC.md:518-519), so p2m_query shards
+// rows evenly over the engine's devices, one host thread per device, with no collective on the hot
+// path; counters are summed on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../../include/p2m.h"
+#include "p2m_device.cuh"
+#include "p2m_kernels.cuh"
+
+#define P2M_API extern "C" __attribute__((visibility("default")))
+
+extern "C" void p2m_set_last_error_internal(const char* msg);  // libp2m_host.so
+
+using p2m::dev::D4;
+using p2m::dev::Params;
+
+namespace {
+
+void set_err(const std::string& s) { p2m_set_last_error_internal(s.c_str()); }
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) {                                                                 \
+            set_err(std::string(#x) + ": " + cudaGetErrorString(e_));                            \
+            return P2M_ERR_CUDA;                                                                 \
+        }                                                                                        \
+    } while (0)
+
+// ---- host-side packing --------------------------------------------------------------------
+
+uint64_t lb_left_size(uint64_t n) {
+    if (n <= 1) return 0;
+    int d = 63 - __builtin_clzll(n);
+    uint64_t full = (1ull << d) - 1ull, last = n - full, half = 1ull << (d - 1);
+    return (half - 1ull) + std::min(last, half);
+}
+
+// Left-balanced k-d tree in BFS order: split on the widest axis of the subset's box (lowest axis on
+// ties), the left subtree takes the lb_left_size(m) smallest points under (coordinate, site id).
+// Same definition as the oracle's tree (oracle/p2m_oracle.c orc_kdtree_build).
+void build_kdtree(const double* xyz, uint64_t n, std::vector<uint32_t>& node_site, std::vector<uint8_t>& node_dim) {
+    node_site.assign(n, 0);
+    node_dim.assign(n, 0);
+    std::vector<uint32_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0u);
+    struct T { uint64_t lo, hi, node; };
+    std::vector<T> st;
+    if (n) st.push_back({0, n, 0});
+    while (!st.empty()) {
+        T t = st.back();
+        st.pop_back();
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (uint64_t i = t.lo; i < t.hi; ++i)
+            for (int k = 0; k < 3; ++k) {
+                double v = xyz[3 * (uint64_t)idx[i] + k];
+                lo[k] = std::min(lo[k], v);
+                hi[k] = std::max(hi[k], v);
+            }
+        int dim = 0;
+        double ext = hi[0] - lo[0];
+        if (hi[1] - lo[1] > ext) { dim = 1; ext = hi[1] - lo[1]; }
+        if (hi[2] - lo[2] > ext) dim = 2;
+        const uint64_t m = t.hi - t.lo, l = lb_left_size(m);
+        std::nth_element(idx.begin() + t.lo, idx.begin() + t.lo + l, idx.begin() + t.hi, [&](uint32_t a, uint32_t b) {
+            double ka = xyz[3 * (uint64_t)a + dim], kb = xyz[3 * (uint64_t)b + dim];
+            return ka < kb || (ka == kb && a < b);
+        });
+        node_site[t.node] = idx[t.lo + l];
+        node_dim[t.node] = (uint8_t)dim;
+        if (t.hi > t.lo + l + 1) st.push_back({t.lo + l + 1, t.hi, 2 * t.node + 2});
+        if (l > 0) st.push_back({t.lo, t.lo + l, 2 * t.node + 1});
+    }
+}
+
+inline double bits_to_double(uint64_t b) { double d; std::memcpy(&d, &b, 8); return d; }
+
+// Fallback BVH: median split of centroids on the longest centroid-box axis, leaf 4, DFS order.
+struct FlatBvh {
+    std::vector<D4> nodes;     // 2 per node
+    std::vector<uint32_t> perm;
+};
+
+void build_bvh(const double* tri, uint64_t nf, FlatBvh& out) {
+    out.nodes.clear();
+    out.perm.resize(nf);
+    std::iota(out.perm.begin(), out.perm.end(), 0u);
+    if (!nf) return;
+    std::vector<double> cen(3 * nf);
+    for (uint64_t f = 0; f < nf; ++f)
+        for (int k = 0; k < 3; ++k) cen[3 * f + k] = (tri[9 * f + k] + tri[9 * f + 3 + k] + tri[9 * f + 6 + k]) * (1.0 / 3.0);
+    struct Rec {
+        FlatBvh& o; const double* tri; const std::vector<double>& cen;
+        uint32_t go(uint32_t lo, uint32_t hi) {
+            uint32_t me = (uint32_t)(o.nodes.size() / 2);
+            o.nodes.push_back(D4{}); o.nodes.push_back(D4{});
+            double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+            double cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (uint32_t i = lo; i < hi; ++i) {
+                uint32_t f = o.perm[i];
+                for (int v = 0; v < 3; ++v)
+                    for (int k = 0; k < 3; ++k) {
+                        double x = tri[9 * (uint64_t)f + 3 * v + k];
+                        bl[k] = std::min(bl[k], x); bh[k] = std::max(bh[k], x);
+                    }
+                for (int k = 0; k < 3; ++k) { cl[k] = std::min(cl[k], cen[3 * (uint64_t)f + k]); ch[k] = std::max(ch[k], cen[3 * (uint64_t)f + k]); }
+            }
+            uint64_t meta;
+            if (hi - lo <= 4) {
+                meta = (uint64_t)(hi - lo) << 32 | lo;
+            } else {
+                int ax = 0;
+                if (ch[1] - cl[1] > ch[ax] - cl[ax]) ax = 1;
+                if (ch[2] - cl[2] > ch[ax] - cl[ax]) ax = 2;
+                uint32_t mid = lo + (hi - lo) / 2;
+                std::nth_element(o.perm.begin() + lo, o.perm.begin() + mid, o.perm.begin() + hi, [&](uint32_t a, uint32_t b) {
+                    double x = cen[3 * (uint64_t)a + ax], y = cen[3 * (uint64_t)b + ax];
+                    return x < y || (x == y && a < b);
+                });
+                go(lo, mid);
+                uint32_t r = go(mid, hi);
+                meta = r;
+            }
+            o.nodes[2 * me] = D4{bl[0], bl[1], bl[2], bh[0]};
+            o.nodes[2 * me + 1] = D4{bh[1], bh[2], bits_to_double(meta), 0.0};
+            return me;
+        }
+    } rec{out, tri, cen};
+    rec.go(0, (uint32_t)nf);
+}
+
+struct Slot {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
+    uint64_t* off = nullptr;
+    uint32_t *lf = nullptr, *bvh_perm = nullptr;
+    Params params{};
+    std::mutex mu;
+    // host-API workspace
+    double *q = nullptr, *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
+    uint64_t cap = 0;
+    unsigned long long* agg = nullptr;
+    // profiling: ring of event quadruples, read lazily by p2m_last_timings (no host sync per call)
+    static constexpr int kRing = 256;
+    std::vector<cudaEvent_t> ev;  // 4 per ring entry
+    int recorded = 0;
+};
+
+}  // namespace
+
+struct p2m_engine {
+    std::vector<std::unique_ptr<Slot>> slots;
+    double replicate_ms = 0.0;
+    uint64_t bytes = 0;
+    bool profiling = false;
+    uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0;
+};
+
+namespace {
+
+void free_slot(Slot& s) {
+    cudaSetDevice(s.dev);
+    cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
+    cudaFree(s.q); cudaFree(s.dist); cudaFree(s.cp); cudaFree(s.face); cudaFree(s.site); cudaFree(s.flags);
+    cudaFree(s.agg);
+    for (auto& e : s.ev) if (e) cudaEventDestroy(e);
+    s.ev.clear();
+    if (s.stream) cudaStreamDestroy(s.stream);
+}
+
+int alloc_slot(Slot& s, const p2m_engine& E) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
+    CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
+    CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
+    CK(cudaMalloc(&s.bvh_perm, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.agg, sizeof(unsigned long long) * 8));
+    s.ev.assign(4 * Slot::kRing, nullptr);
+    for (auto& e : s.ev) CK(cudaEventCreate(&e));
+    // keep the stream-ordered pool's memory between calls (the per-call sort workspace)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, s.dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return P2M_OK;
+}
+
+int ensure_ws(Slot& s, uint64_t n) {
+    if (n <= s.cap) return P2M_OK;
+    cudaFree(s.q); cudaFree(s.dist); cudaFree(s.cp); cudaFree(s.face); cudaFree(s.site); cudaFree(s.flags);
+    s.cap = 0;
+    CK(cudaMalloc(&s.q, 24 * n));
+    CK(cudaMalloc(&s.dist, 8 * n));
+    CK(cudaMalloc(&s.cp, 24 * n));
+    CK(cudaMalloc(&s.face, 4 * n));
+    CK(cudaMalloc(&s.site, 4 * n));
+    CK(cudaMalloc(&s.flags, 4 * n));
+    s.cap = n;
+    return P2M_OK;
+}
+
+// Morton keys -> sort -> fused query.  rows_out (optional) receives the sorted row order.
+int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2m::dev::Out& o, bool counters,
+                 cudaStream_t st, bool nearest_only, uint32_t* d_site_only) {
+    if (n >= (1ull << 32)) { set_err("p2m_query_device: at most 2^32-1 rows per call"); return P2M_ERR_INVALID; }
+    CK(cudaSetDevice(s.dev));
+    uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
+    CK(cudaMallocAsync(&keys, 4 * n, st));
+    CK(cudaMallocAsync(&rows, 4 * n, st));
+    CK(cudaMallocAsync(&keys2, 4 * n, st));
+    CK(cudaMallocAsync(&rows2, 4 * n, st));
+    CK(cudaMallocAsync(&tmp, tb, st));
+    const bool prof = E->profiling && s.recorded < Slot::kRing;
+    cudaEvent_t* ev = prof ? &s.ev[4 * s.recorded] : nullptr;
+    if (prof) { CK(cudaEventRecord(ev[0], st)); ++s.recorded; }
+    CK(p2m::dev::launch_morton(d_q, n, s.params, keys, rows, st));
+    if (prof) CK(cudaEventRecord(ev[1], st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
+    if (prof) CK(cudaEventRecord(ev[2], st));
+    if (nearest_only) CK(p2m::dev::launch_nearest(s.params, d_q, rows2, n, d_site_only, st));
+    else CK(p2m::dev::launch_query(s.params, d_q, rows2, n, o, counters, st));
+    if (prof) CK(cudaEventRecord(ev[3], st));
+    CK(cudaFreeAsync(keys, st));
+    CK(cudaFreeAsync(rows, st));
+    CK(cudaFreeAsync(keys2, st));
+    CK(cudaFreeAsync(rows2, st));
+    CK(cudaFreeAsync(tmp, st));
+    return P2M_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+
+P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int* device_ids, p2m_engine** out) {
+    if (!d || !out || n_devices < 1 || !d->site_xyz || !d->site_kind || !d->tri_xyz || !d->face_sphere ||
+        !d->list_offsets || (!d->list_faces && d->list_offsets[d->n_sites] > 0)) {
+        set_err("p2m_engine_create: invalid descriptor");
+        return P2M_ERR_INVALID;
+    }
+    if (d->n_sites == 0 || d->n_faces == 0 || d->n_sites >= (1ull << 32) || d->n_faces >= (1ull << 32)) {
+        set_err("p2m_engine_create: engine not built (no sites/faces) or too large");
+        return P2M_ERR_NOT_BUILT;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        set_err("p2m_engine_create: no CUDA device available");
+        return P2M_ERR_CUDA;
+    }
+    const uint64_t S = d->n_sites, F = d->n_faces, L = d->list_offsets[S];
+    for (uint64_t s = 0; s < S; ++s)
+        if (d->list_offsets[s] > d->list_offsets[s + 1]) { set_err("p2m_engine_create: offsets not monotone"); return P2M_ERR_INVALID; }
+    for (uint64_t j = 0; j < L; ++j)
+        if (d->list_faces[j] >= F) { set_err("p2m_engine_create: list face id out of range"); return P2M_ERR_INVALID; }
+
+    auto E = std::make_unique<p2m_engine>();
+    E->n_sites = S; E->n_faces = F; E->n_entries = L;
+
+    // ---- pack ----
+    std::vector<uint32_t> node_site;
+    std::vector<uint8_t> node_dim;
+    build_kdtree(d->site_xyz, S, node_site, node_dim);
+    std::vector<D4> kd(S);
+    double klo[3] = {INFINITY, INFINITY, INFINITY}, khi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint64_t k = 0; k < S; ++k) {
+        const uint32_t id = node_site[k];
+        const double* p = d->site_xyz + 3 * (uint64_t)id;
+        uint64_t meta = (uint64_t)id | (uint64_t)node_dim[k] << 32 |
+                        (d->site_kind[id] == P2M_SITE_SENTINEL ? (1ull << 34) : 0ull);
+        kd[k] = D4{p[0], p[1], p[2], bits_to_double(meta)};
+        if (d->site_kind[id] != P2M_SITE_SENTINEL)
+            for (int c = 0; c < 3; ++c) { klo[c] = std::min(klo[c], p[c]); khi[c] = std::max(khi[c], p[c]); }
+    }
+    std::vector<D4> rec(4 * F);
+    for (uint64_t f = 0; f < F; ++f) {
+        const double* t = d->tri_xyz + 9 * f;
+        const double* s = d->face_sphere + 4 * f;
+        rec[4 * f] = D4{s[0], s[1], s[2], s[3]};
+        rec[4 * f + 1] = D4{t[0], t[1], t[2], t[3]};
+        rec[4 * f + 2] = D4{t[4], t[5], t[6], t[7]};
+        rec[4 * f + 3] = D4{t[8], 0.0, 0.0, 0.0};
+    }
+    FlatBvh bvh;
+    build_bvh(d->tri_xyz, F, bvh);
+    E->n_bvh = bvh.nodes.size() / 2;
+
+    Params P{};
+    P.n_nodes = (uint32_t)S;
+    P.n_faces = (uint32_t)F;
+    double dd2 = 0.0;
+    {
+        double dx = d->domain_max[0] - d->domain_min[0], dy = d->domain_max[1] - d->domain_min[1],
+               dz = d->domain_max[2] - d->domain_min[2];
+        dd2 = dx * dx + dy * dy + dz * dz;
+    }
+    P.prune_eps = 1e-9 * std::sqrt(dd2);  // same definition as the oracle (orc_ctx_create)
+    for (int c = 0; c < 3; ++c) {
+        P.dmin[c] = d->domain_min[c];
+        P.dmax[c] = d->domain_max[c];
+        if (!(klo[c] <= khi[c])) { klo[c] = d->domain_min[c]; khi[c] = d->domain_max[c]; }
+        double mid = 0.5 * (klo[c] + khi[c]), h = 0.75 * (khi[c] - klo[c]);
+        if (!(h > 0)) h = 1.0;
+        P.key_lo[c] = mid - h;
+        P.key_scale[c] = 1024.0 / (2.0 * h);
+    }
+
+    // ---- upload to the first device, peer-replicate to the rest ----
+    for (int k = 0; k < n_devices; ++k) {
+        auto s = std::make_unique<Slot>();
+        s->dev = device_ids ? device_ids[k] : k;
+        if (s->dev < 0 || s->dev >= ndev) { set_err("p2m_engine_create: bad device id"); return P2M_ERR_INVALID; }
+        E->slots.push_back(std::move(s));
+    }
+    for (auto& s : E->slots) {
+        int rc = alloc_slot(*s, *E);
+        if (rc != P2M_OK) { for (auto& x : E->slots) free_slot(*x); return rc; }
+    }
+    Slot& s0 = *E->slots[0];
+    auto fail = [&](int rc) { for (auto& x : E->slots) free_slot(*x); return rc; };
+    {
+        cudaSetDevice(s0.dev);
+        if (cudaMemcpy(s0.kd, kd.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.rec, rec.data(), sizeof(D4) * 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+            (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
+            cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess) {
+            set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
+            return fail(P2M_ERR_CUDA);
+        }
+    }
+    E->bytes = sizeof(D4) * (S + 4 * F + bvh.nodes.size()) + 8 * (S + 1) + 4 * (L + F);
+    auto t0 = std::chrono::steady_clock::now();
+    for (size_t k = 1; k < E->slots.size(); ++k) {
+        Slot& s = *E->slots[k];
+        cudaSetDevice(s.dev);
+        if (s.dev != s0.dev) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, s.dev, s0.dev);
+            if (can) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(s0.dev, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) { set_err("peer access failed"); return fail(P2M_ERR_CUDA); }
+                cudaGetLastError();
+            }
+        }
+        struct { void* dst; const void* src; size_t n; } cp[] = {
+            {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.off, s0.off, 8 * (S + 1)},
+            {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F}};
+        for (auto& c : cp)
+            if (c.n && cudaMemcpyPeerAsync(c.dst, s.dev, c.src, s0.dev, c.n, s.stream) != cudaSuccess) {
+                set_err("p2m_engine_create: peer copy failed");
+                return fail(P2M_ERR_CUDA);
+            }
+    }
+    for (auto& s : E->slots) {
+        cudaSetDevice(s->dev);
+        if (cudaStreamSynchronize(s->stream) != cudaSuccess) { set_err("p2m_engine_create: replica sync failed"); return fail(P2M_ERR_CUDA); }
+    }
+    E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& s : E->slots) {
+        s->params = P;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm;
+    }
+    *out = E.release();
+    return P2M_OK;
+}
+
+P2M_API void p2m_engine_destroy(p2m_engine* e) {
+    if (!e) return;
+    for (auto& s : e->slots) free_slot(*s);
+    delete e;
+}
+
+P2M_API int p2m_engine_info(const p2m_engine* e, int* n, double* ms, uint64_t* bytes) {
+    if (!e) { set_err("p2m_engine_info: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (n) *n = (int)e->slots.size();
+    if (ms) *ms = e->replicate_ms;
+    if (bytes) *bytes = e->bytes;
+    return P2M_OK;
+}
+
+P2M_API int p2m_query_device(p2m_engine* e, int slot, const double* d_q, uint64_t n, double* d_dist, double* d_cp,
+                             uint32_t* d_face, uint32_t* d_site, uint32_t* d_flags, void* stream, p2m_counters* cnt) {
+    if (!e) { set_err("p2m_query_device: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (slot < 0 || slot >= (int)e->slots.size()) { set_err("p2m_query_device: bad slot"); return P2M_ERR_INVALID; }
+    if (n && (!d_q || !d_dist || !d_cp || !d_face || !d_site)) { set_err("p2m_query_device: null buffer"); return P2M_ERR_INVALID; }
+    Slot& s = *e->slots[slot];
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cnt) std::memset(cnt, 0, sizeof *cnt);
+    if (!n) return P2M_OK;
+    p2m::dev::Out o{d_dist, d_cp, d_face, d_site, d_flags, nullptr, nullptr};
+    std::unique_lock<std::mutex> lk(s.mu, std::defer_lock);
+    if (cnt) {
+        lk.lock();
+        CK(cudaSetDevice(s.dev));
+        CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, st));
+        o.agg = s.agg;
+    }
+    int rc = run_pipeline(e, s, d_q, n, o, cnt != nullptr, st, false, nullptr);
+    if (rc != P2M_OK) return rc;
+    if (cnt) {
+        unsigned long long h[8];
+        CK(cudaMemcpyAsync(h, s.agg, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cnt->n_queries = n;
+        cnt->candidates_visited = h[0];
+        cnt->exact_evaluations = h[1];
+        cnt->pruned = h[0] - h[1];
+        cnt->kd_nodes_visited = h[2];
+        cnt->fallbacks = h[3];
+    }
+    return P2M_OK;
+}
+
+P2M_API int p2m_nearest_site_device(p2m_engine* e, int slot, const double* d_q, uint64_t n, uint32_t* d_site, void* stream) {
+    if (!e) { set_err("p2m_nearest_site_device: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (slot < 0 || slot >= (int)e->slots.size()) { set_err("bad slot"); return P2M_ERR_INVALID; }
+    if (!n) return P2M_OK;
+    p2m::dev::Out o{};
+    return run_pipeline(e, *e->slots[slot], d_q, n, o, false, (cudaStream_t)stream, true, d_site);
+}
+
+P2M_API int p2m_query_device_counters(p2m_engine* e, int slot, const double* d_q, uint64_t n, uint64_t* d_pq, void* stream) {
+    if (!e) { set_err("p2m_query_device_counters: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (slot < 0 || slot >= (int)e->slots.size()) { set_err("bad slot"); return P2M_ERR_INVALID; }
+    if (!n) return P2M_OK;
+    Slot& s = *e->slots[slot];
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaSetDevice(s.dev));
+    double *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr;
+    CK(cudaMallocAsync(&dist, 8 * n, st));
+    CK(cudaMallocAsync(&cp, 24 * n, st));
+    CK(cudaMallocAsync(&face, 4 * n, st));
+    CK(cudaMallocAsync(&site, 4 * n, st));
+    p2m::dev::Out o{dist, cp, face, site, nullptr, d_pq, nullptr};
+    int rc = run_pipeline(e, s, d_q, n, o, true, st, false, nullptr);
+    cudaFreeAsync(dist, st); cudaFreeAsync(cp, st); cudaFreeAsync(face, st); cudaFreeAsync(site, st);
+    return rc;
+}
+
+P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, double* cp, uint32_t* face,
+                      uint32_t* site, uint32_t* flags, p2m_counters* cnt) {
+    if (!e) { set_err("p2m_query: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (n && (!q || !dist || !cp || !face || !site)) { set_err("p2m_query: null buffer"); return P2M_ERR_INVALID; }
+    if (cnt) std::memset(cnt, 0, sizeof *cnt);
+    if (!n) return P2M_OK;
+    const int G = (int)e->slots.size();
+    std::vector<int> rcs(G, P2M_OK);
+    std::vector<p2m_counters> parts(G);
+    std::vector<std::string> errs(G);
+    auto work = [&](int g) {
+        const uint64_t b = n * (uint64_t)g / G, en = n * (uint64_t)(g + 1) / G, m = en - b;
+        parts[g] = p2m_counters{};
+        if (!m) return;
+        Slot& s = *e->slots[g];
+        std::lock_guard<std::mutex> lk(s.mu);
+        auto run = [&]() -> int {
+            CK(cudaSetDevice(s.dev));
+            int rc = ensure_ws(s, m);
+            if (rc != P2M_OK) return rc;
+            CK(cudaMemcpyAsync(s.q, q + 3 * b, 24 * m, cudaMemcpyHostToDevice, s.stream));
+            p2m::dev::Out o{s.dist, s.cp, s.face, s.site, s.flags, nullptr, cnt ? s.agg : nullptr};
+            if (cnt) CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.stream));
+            rc = run_pipeline(e, s, s.q, m, o, cnt != nullptr, s.stream, false, nullptr);
+            if (rc != P2M_OK) return rc;
+            CK(cudaMemcpyAsync(dist + b, s.dist, 8 * m, cudaMemcpyDeviceToHost, s.stream));
+            CK(cudaMemcpyAsync(cp + 3 * b, s.cp, 24 * m, cudaMemcpyDeviceToHost, s.stream));
+            CK(cudaMemcpyAsync(face + b, s.face, 4 * m, cudaMemcpyDeviceToHost, s.stream));
+            CK(cudaMemcpyAsync(site + b, s.site, 4 * m, cudaMemcpyDeviceToHost, s.stream));
+            if (flags) CK(cudaMemcpyAsync(flags + b, s.flags, 4 * m, cudaMemcpyDeviceToHost, s.stream));
+            unsigned long long h[8] = {0};
+            if (cnt) CK(cudaMemcpyAsync(h, s.agg, sizeof h, cudaMemcpyDeviceToHost, s.stream));
+            CK(cudaStreamSynchronize(s.stream));
+            parts[g].n_queries = m;
+            parts[g].candidates_visited = h[0];
+            parts[g].exact_evaluations = h[1];
+            parts[g].pruned = h[0] - h[1];
+            parts[g].kd_nodes_visited = h[2];
+            parts[g].fallbacks = h[3];
+            return P2M_OK;
+        };
+        rcs[g] = run();
+        if (rcs[g] != P2M_OK) errs[g] = p2m_last_error();
+    };
+    if (G == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int g = 0; g < G; ++g) th.emplace_back(work, g);
+        for (auto& t : th) t.join();
+    }
+    for (int g = 0; g < G; ++g)
+        if (rcs[g] != P2M_OK) { set_err(errs[g]); return rcs[g]; }
+    if (cnt) {
+        for (auto& c : parts) {
+            cnt->n_queries += c.n_queries;
+            cnt->candidates_visited += c.candidates_visited;
+            cnt->exact_evaluations += c.exact_evaluations;
+            cnt->pruned += c.pruned;
+            cnt->kd_nodes_visited += c.kd_nodes_visited;
+            cnt->fallbacks += c.fallbacks;
+        }
+    }
+    return P2M_OK;
+}
+
+P2M_API int p2m_set_profiling(p2m_engine* e, int enable) {
+    if (!e) { set_err("engine not built"); return P2M_ERR_NOT_BUILT; }
+    e->profiling = enable != 0;
+    for (auto& s : e->slots) s->recorded = 0;
+    return P2M_OK;
+}
+
+// Mean per-call split over the calls recorded since profiling was (re)enabled; resets the ring.
+P2M_API int p2m_last_timings(p2m_engine* e, int slot, float* ms4) {
+    if (!e || !ms4 || slot < 0 || slot >= (int)e->slots.size()) { set_err("p2m_last_timings: bad argument"); return P2M_ERR_INVALID; }
+    Slot& s = *e->slots[slot];
+    double acc[4] = {0, 0, 0, 0};
+    CK(cudaSetDevice(s.dev));
+    for (int r = 0; r < s.recorded; ++r) {
+        cudaEvent_t* ev = &s.ev[4 * r];
+        CK(cudaEventSynchronize(ev[3]));
+        float m;
+        CK(cudaEventElapsedTime(&m, ev[0], ev[1])); acc[0] += m;
+        CK(cudaEventElapsedTime(&m, ev[1], ev[2])); acc[1] += m;
+        CK(cudaEventElapsedTime(&m, ev[2], ev[3])); acc[2] += m;
+        CK(cudaEventElapsedTime(&m, ev[0], ev[3])); acc[3] += m;
+    }
+    for (int k = 0; k < 4; ++k) ms4[k] = s.recorded ? (float)(acc[k] / s.recorded) : 0.0f;
+    s.recorded = 0;
+    return P2M_OK;
+}
+
+// Count the kernels one p2m_query_device call launches by capturing it into a CUDA graph.
+P2M_API int p2m_kernels_per_query(p2m_engine* e, uint64_t n, int* launches) {
+    if (!e || !launches) { set_err("p2m_kernels_per_query: bad argument"); return P2M_ERR_INVALID; }
+    Slot& s = *e->slots[0];
+    CK(cudaSetDevice(s.dev));
+    if (!n) n = 1;
+    double *q = nullptr, *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr;
+    CK(cudaMalloc(&q, 24 * n)); CK(cudaMemset(q, 0, 24 * n));
+    CK(cudaMalloc(&dist, 8 * n)); CK(cudaMalloc(&cp, 24 * n)); CK(cudaMalloc(&face, 4 * n)); CK(cudaMalloc(&site, 4 * n));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    bool prof = e->profiling;
+    e->profiling = false;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    p2m::dev::Out o{dist, cp, face, site, nullptr, nullptr, nullptr};
+    int rc = run_pipeline(e, s, q, n, o, false, st, false, nullptr);
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(st, &g);
+    e->profiling = prof;
+    int k = 0;
+    if (rc == P2M_OK && g) {
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (auto& x : nodes) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(x, &t);
+            if (t == cudaGraphNodeTypeKernel) ++k;
+        }
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(st);
+    cudaFree(q); cudaFree(dist); cudaFree(cp); cudaFree(face); cudaFree(site);
+    if (rc != P2M_OK) return rc;
+    *launches = k;
+    return P2M_OK;
+}

@@ -1,0 +1,41 @@
+"""GPU parity: the CUDA query path (through the C ABI) vs the CPU oracle on identical inputs.
+
+Bar (BASELINE.json north_star): site and face ids exact, distance and closest point within 1e-6
+relative.  fp64 with --fmad=false and the reference's operation order makes the whole row
+bit-identical, which is what these tests assert (tolerance 0)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_00429_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(r, ref, n):
+    for k in ("site", "face", "flags"):
+        a, b = getattr(r, k), ref[k]
+        bad = np.flatnonzero(a != b)
+        assert len(bad) == 0, f"{k}: {len(bad)} of {n} rows differ, first {bad[:5]}"
+    for k in ("distance", "closest"):
+        a, b = getattr(r, k), ref[k]
+        assert a.tobytes() == b.tobytes(), f"{k} not bit-identical (max rel {np.nanmax(np.abs(a-b)/np.maximum(np.abs(b),1e-300))})"
+
+
+@pytest.mark.parametrize("fixture,nq,cfg", [("ico3", 20000, None), ("c1", 200000, 1), ("c2", 200000, 2)])
+def test_parity_vs_oracle(request, fixture, nq, cfg):
+    V, F, h = request.getfixturevalue(fixture)
+    if cfg is None:
+        q = np.random.default_rng(3).uniform(-1.3, 1.3, size=(nq, 3))
+    else:
+        q = P.gen_queries(cfg, V, F, 0, nq)
+    eng = P.Engine(h)
+    r = eng.batch_query(q)
+    ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
+    _compare(r, ref, nq)
+    # counters: candidates and kd nodes are deterministic; exact evaluations equal for the sequential scan
+    c, rc = r.counters, ref["counters"]
+    assert c["candidates_visited"] == rc["candidates_visited"]
+    assert c["kd_nodes_visited"] == rc["kd_nodes_visited"]
+    assert c["exact_evaluations"] == rc["exact_evaluations"]
+    assert c["fallbacks"] == rc["fallbacks"]
