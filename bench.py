@@ -188,6 +188,7 @@ def main():
     ap.add_argument("--aux-corner-union", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--scan-mode", type=int, default=0, help="0 grouped (default), 1 fused per-row")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -215,6 +216,7 @@ def main():
     st = h.stats()
     eng = P.Engine(h, devices=[dev])
     lib = L.cuda()
+    L.check(lib.p2m_set_scan_mode(eng.handle, args.scan_mode))
 
     stream = torch.cuda.current_stream()
     sptr = C.c_void_p(stream.cuda_stream)
@@ -259,7 +261,7 @@ def main():
         if world > 1:
             dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    split = (C.c_float * 4)()
+    split = (C.c_float * 6)()
     L.check(lib.p2m_last_timings(eng.handle, 0, split))
     L.check(lib.p2m_set_profiling(eng.handle, 0))
     split = [float(x) for x in split]
@@ -304,8 +306,12 @@ def main():
         return
 
     peak, peak_src = peaks()
-    t_query_s = split[2] / 1e3 if split[2] > 0 else ms / 1e3
-    achieved = B_alg / t_query_s / 1e9
+    # dominant kernel = the grouped list scan; its algorithmic bytes exclude the k-d descent
+    # (that is the descend kernel's): 24 q + 40 out + 8 offsets + 36 C_q + 72 E_q per query
+    B_scan = B_alg - 32 * c["kd_nodes_visited"]
+    t_scan_s = split[4] / 1e3 if split[4] > 0 else ms / 1e3
+    achieved = B_scan / t_scan_s / 1e9
+    pipeline_gbs = B_alg / (split[5] / 1e3 if split[5] > 0 else ms / 1e3) / 1e9
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_c{cfg}.json")
     if os.path.exists(tr_path):
@@ -330,12 +336,14 @@ def main():
             "list_max": st["list_max"],
             "per_query": {"candidates": c["candidates_visited"] / n, "exact": c["exact_evaluations"] / n,
                           "kd_nodes": c["kd_nodes_visited"] / n, "fallbacks": c["fallbacks"]},
-            "split_ms": {"morton": split[0], "sort": split[1], "query": split[2], "total": split[3]},
+            "split_ms": {"morton": split[0], "sort": split[1], "descend": split[2], "regroup_sort": split[3], "scan": split[4], "total": split[5]},
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_query (fused nearest-site descent + pruned list scan)",
-                     "algorithmic_bytes_per_launch": B_alg,
-                     "bytes_per_query": "72 + 32 n_q + 36 C_q + 72 E_q (SURVEY.md 8(d))", "peak_source": peak_src},
+                     "traffic": traffic, "kernel": "k_scan_grouped (site-tiled pruned list scan, exact fp64)",
+                     "algorithmic_bytes_per_launch": B_scan,
+                     "bytes_per_query": "72 + 36 C_q + 72 E_q (SURVEY.md 8(d) minus the 32 n_q of the descent kernel)",
+                     "pipeline_algorithmic_gbs": pipeline_gbs, "pipeline_bytes_per_step": B_alg,
+                     "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": 24 * n,
                 "d2h_bytes_per_step": 44 * n, "api": "p2m_query (host pinned buffers, synchronous)",
                 "rows_equal_device_path": same},

@@ -124,10 +124,18 @@ int p2m_query_device_counters(p2m_engine *engine, int slot, const double *d_q_xy
                               uint64_t *d_per_query, void *stream);
 
 /* Kernel-split timing (ms, CUDA events recorded on each call's own stream, no host sync):
- * [0] morton keys, [1] sort, [2] fused query, [3] total -- mean over the p2m_query_device calls
- * recorded since p2m_set_profiling(e, 1) (up to 256), then the record is reset. */
+ * ms[0] morton keys, [1] Morton sort, [2] nearest-site descent (or the whole fused query),
+ * [3] regroup sort, [4] grouped list scan, [5] total -- mean over the p2m_query_device calls
+ * recorded since p2m_set_profiling(e, 1) (up to 256), then the record is reset.  ms has 6 slots. */
 int p2m_set_profiling(p2m_engine *engine, int enable);
-int p2m_last_timings(p2m_engine *engine, int slot, float *ms4);
+int p2m_last_timings(p2m_engine *engine, int slot, float *ms);
+
+/* Scan strategy (results are identical; counters too):
+ *   P2M_SCAN_GROUPED (default) -- descend, regroup rows by nearest site, scan each site's list once
+ *                                  per 256-row tile from shared memory
+ *   P2M_SCAN_FUSED             -- one thread per row does descent + scan from global memory */
+enum { P2M_SCAN_GROUPED = 0, P2M_SCAN_FUSED = 1 };
+int p2m_set_scan_mode(p2m_engine *engine, int mode);
 
 /* Number of kernels launched by one p2m_query_device call of n rows (for gpu_launches). */
 int p2m_kernels_per_query(p2m_engine *engine, uint64_t n, int *launches);

@@ -162,6 +162,7 @@ def cuda() -> C.CDLL:
         L.p2m_set_profiling.argtypes = [vp, C.c_int]
         L.p2m_last_timings.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
         L.p2m_kernels_per_query.argtypes = [vp, C.c_uint64, C.POINTER(C.c_int)]
+        L.p2m_set_scan_mode.argtypes = [vp, C.c_int]
         _cuda = L
     return _cuda
 

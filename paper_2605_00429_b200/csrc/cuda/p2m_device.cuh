@@ -95,6 +95,9 @@ struct Params {
     double dmin[3], dmax[3];
     double prune_eps;
     double key_lo[3], key_scale[3];  // Morton key box
+    float f32_delta;        // additive slack of the conservative fp32 sphere pre-filter
+    const uint8_t* heavy;   // per site: 1 if its rows are tiled long_tile rows per CTA
+    uint32_t long_tile;     // (32, 64, 128 or 256)
 };
 
 }  // namespace dev

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -153,6 +154,7 @@ struct Slot {
     D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
     uint64_t* off = nullptr;
     uint32_t *lf = nullptr, *bvh_perm = nullptr;
+    uint8_t* heavy = nullptr;
     Params params{};
     std::mutex mu;
     // host-API workspace
@@ -160,9 +162,10 @@ struct Slot {
     uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
     uint64_t cap = 0;
     unsigned long long* agg = nullptr;
-    // profiling: ring of event quadruples, read lazily by p2m_last_timings (no host sync per call)
+    // profiling: ring of event sets, read lazily by p2m_last_timings (no host sync per call)
     static constexpr int kRing = 256;
-    std::vector<cudaEvent_t> ev;  // 4 per ring entry
+    static constexpr int kEv = 6;  // morton | sort | descend | regroup sort | scan | end
+    std::vector<cudaEvent_t> ev;   // kEv per ring entry
     int recorded = 0;
 };
 
@@ -173,7 +176,8 @@ struct p2m_engine {
     double replicate_ms = 0.0;
     uint64_t bytes = 0;
     bool profiling = false;
-    uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0;
+    int scan_mode = P2M_SCAN_GROUPED;
+    uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
 };
 
 namespace {
@@ -181,6 +185,7 @@ namespace {
 void free_slot(Slot& s) {
     cudaSetDevice(s.dev);
     cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
+    cudaFree(s.heavy);
     cudaFree(s.q); cudaFree(s.dist); cudaFree(s.cp); cudaFree(s.face); cudaFree(s.site); cudaFree(s.flags);
     cudaFree(s.agg);
     for (auto& e : s.ev) if (e) cudaEventDestroy(e);
@@ -198,7 +203,9 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
     CK(cudaMalloc(&s.bvh_perm, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.agg, sizeof(unsigned long long) * 8));
-    s.ev.assign(4 * Slot::kRing, nullptr);
+    CK(cudaMalloc(&s.heavy, std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMemset(s.heavy, 0, std::max<uint64_t>(1, E.n_sites)));
+    s.ev.assign(Slot::kEv * Slot::kRing, nullptr);
     for (auto& e : s.ev) CK(cudaEventCreate(&e));
     // keep the stream-ordered pool's memory between calls (the per-call sort workspace)
     cudaMemPool_t pool;
@@ -230,28 +237,102 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
     CK(cudaSetDevice(s.dev));
     uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
     void* tmp = nullptr;
+    uint32_t *flag = nullptr, *tix = nullptr, *tiles = nullptr, *meta = nullptr;
+    const bool grouped = !nearest_only && E->scan_mode == P2M_SCAN_GROUPED;
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
+    tb = std::max(tb, p2m::dev::tiles_tmp_bytes(n));
     CK(cudaMallocAsync(&keys, 4 * n, st));
     CK(cudaMallocAsync(&rows, 4 * n, st));
     CK(cudaMallocAsync(&keys2, 4 * n, st));
     CK(cudaMallocAsync(&rows2, 4 * n, st));
     CK(cudaMallocAsync(&tmp, tb, st));
+    if (grouped) {
+        CK(cudaMallocAsync(&flag, 4 * n, st));
+        CK(cudaMallocAsync(&tix, 4 * n, st));
+        CK(cudaMallocAsync(&tiles, 4 * p2m::dev::max_tiles(n, E->n_sites), st));
+        CK(cudaMallocAsync(&meta, 16, st));
+    }
     const bool prof = E->profiling && s.recorded < Slot::kRing;
-    cudaEvent_t* ev = prof ? &s.ev[4 * s.recorded] : nullptr;
+    cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * s.recorded] : nullptr;
     if (prof) { CK(cudaEventRecord(ev[0], st)); ++s.recorded; }
     CK(p2m::dev::launch_morton(d_q, n, s.params, keys, rows, st));
     if (prof) CK(cudaEventRecord(ev[1], st));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
     if (prof) CK(cudaEventRecord(ev[2], st));
-    if (nearest_only) CK(p2m::dev::launch_nearest(s.params, d_q, rows2, n, d_site_only, st));
-    else CK(p2m::dev::launch_query(s.params, d_q, rows2, n, o, counters, st));
-    if (prof) CK(cudaEventRecord(ev[3], st));
+    if (nearest_only) {
+        CK(p2m::dev::launch_nearest(s.params, d_q, rows2, n, d_site_only, st));
+        if (prof) for (int k = 3; k < Slot::kEv; ++k) CK(cudaEventRecord(ev[k], st));
+    } else if (E->scan_mode == P2M_SCAN_FUSED) {
+        CK(p2m::dev::launch_query(s.params, d_q, rows2, n, o, counters, st));
+        if (prof) for (int k = 3; k < Slot::kEv; ++k) CK(cudaEventRecord(ev[k], st));
+    } else {
+        // descend in Morton order (keys buffer reused for the site keys), regroup by site (stable),
+        // then scan per site tile
+        CK(p2m::dev::launch_descend(s.params, d_q, rows2, n, keys, o, counters, st));
+        if (prof) CK(cudaEventRecord(ev[3], st));
+        const int bits = std::max(1, 64 - __builtin_clzll((unsigned long long)E->n_sites));  // keys <= n_sites
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows2, rows, (int64_t)n, 0, bits, st));
+        // tiles over the site-sorted order (keys / rows2 are free again: hpos / run starts)
+        CK(p2m::dev::launch_tiles(s.params, keys2, n, (uint32_t)E->n_sites, keys, rows2, flag, tix, tiles, meta, tmp, tb, st));
+        if (prof) CK(cudaEventRecord(ev[4], st));
+        CK(p2m::dev::launch_scan_tiles(s.params, d_q, rows, keys2, tiles, meta, n, o, counters, st));
+        if (prof) CK(cudaEventRecord(ev[5], st));
+    }
     CK(cudaFreeAsync(keys, st));
     CK(cudaFreeAsync(rows, st));
     CK(cudaFreeAsync(keys2, st));
     CK(cudaFreeAsync(rows2, st));
     CK(cudaFreeAsync(tmp, st));
+    if (grouped) {
+        CK(cudaFreeAsync(flag, st));
+        CK(cudaFreeAsync(tix, st));
+        CK(cudaFreeAsync(tiles, st));
+        CK(cudaFreeAsync(meta, st));
+    }
+    return P2M_OK;
+}
+
+// Per-site exact-work estimate: query every site's own position once with the sequential (fused)
+// scan and count the exact point-triangle evaluations.  Sites whose estimate reaches the threshold
+// (deep auxiliary sites of closed surfaces, where the distance field is flat and sphere pruning
+// cannot cut the list) get short tiles so their rows spread over many SMs.
+int mark_heavy_sites(p2m_engine* E, const p2m_engine_desc* d) {
+    uint32_t thr = 1024;
+    if (const char* v = std::getenv("P2M_HEAVY_E")) thr = (uint32_t)std::strtoul(v, nullptr, 10);
+    const uint64_t S = E->n_sites;
+    Slot& s0 = *E->slots[0];
+    CK(cudaSetDevice(s0.dev));
+    double *q = nullptr, *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr;
+    uint64_t* pq = nullptr;
+    CK(cudaMalloc(&q, 24 * S)); CK(cudaMalloc(&dist, 8 * S)); CK(cudaMalloc(&cp, 24 * S));
+    CK(cudaMalloc(&face, 4 * S)); CK(cudaMalloc(&site, 4 * S)); CK(cudaMalloc(&pq, 24 * S));
+    CK(cudaMemcpy(q, d->site_xyz, 24 * S, cudaMemcpyHostToDevice));
+    const int mode = E->scan_mode;
+    const bool prof = E->profiling;
+    E->scan_mode = P2M_SCAN_FUSED;
+    E->profiling = false;
+    p2m::dev::Out o{dist, cp, face, site, nullptr, pq, nullptr};
+    int rc = run_pipeline(E, s0, q, S, o, true, s0.stream, false, nullptr);
+    E->scan_mode = mode;
+    E->profiling = prof;
+    std::vector<uint64_t> h(3 * S);
+    if (rc == P2M_OK) {
+        CK(cudaStreamSynchronize(s0.stream));
+        CK(cudaMemcpy(h.data(), pq, 24 * S, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(q); cudaFree(dist); cudaFree(cp); cudaFree(face); cudaFree(site); cudaFree(pq);
+    if (rc != P2M_OK) return rc;
+    std::vector<uint8_t> heavy(S, 0);
+    uint64_t n_heavy = 0;
+    for (uint64_t i = 0; i < S; ++i)
+        if (d->site_kind[i] != P2M_SITE_SENTINEL && h[3 * i + 1] >= thr) { heavy[i] = 1; ++n_heavy; }
+    E->n_heavy = n_heavy;
+    for (auto& s : E->slots) {
+        CK(cudaSetDevice(s->dev));
+        CK(cudaMemcpy(s->heavy, heavy.data(), S, cudaMemcpyHostToDevice));
+    }
     return P2M_OK;
 }
 
@@ -322,6 +403,21 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         dd2 = dx * dx + dy * dy + dz * dz;
     }
     P.prune_eps = 1e-9 * std::sqrt(dd2);  // same definition as the oracle (orc_ctx_create)
+    {
+        // fp32 pre-filter slack: coordinates of every scanned query and sphere centre lie in D, so
+        // rounding each to fp32 moves |q - c| by at most 2*sqrt(3)*2^-24*M; doubled, plus 2 eps
+        double M = 0.0;
+        for (int c = 0; c < 3; ++c) M = std::max({M, std::fabs(d->domain_min[c]), std::fabs(d->domain_max[c])});
+        const double delta = 4.0 * std::sqrt(3.0) * std::ldexp(1.0, -24) * M + 2.0 * P.prune_eps;
+        float df = (float)delta;
+        if ((double)df < delta) df = std::nextafter(df, INFINITY);
+        P.f32_delta = df;
+    }
+    P.long_tile = 32;
+    if (const char* v = std::getenv("P2M_LONG_TILE")) {
+        uint32_t t = (uint32_t)std::strtoul(v, nullptr, 10);
+        if (t == 32 || t == 64 || t == 128 || t == 256) P.long_tile = t;
+    }
     for (int c = 0; c < 3; ++c) {
         P.dmin[c] = d->domain_min[c];
         P.dmax[c] = d->domain_max[c];
@@ -388,7 +484,11 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     for (auto& s : E->slots) {
         s->params = P;
         s->params.kd = s->kd; s->params.rec = s->rec; s->params.off = s->off; s->params.lf = s->lf;
-        s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm;
+        s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
+    }
+    {
+        int rc = mark_heavy_sites(E.get(), d);
+        if (rc != P2M_OK) return fail(rc);
     }
     *out = E.release();
     return P2M_OK;
@@ -542,22 +642,27 @@ P2M_API int p2m_set_profiling(p2m_engine* e, int enable) {
 }
 
 // Mean per-call split over the calls recorded since profiling was (re)enabled; resets the ring.
-P2M_API int p2m_last_timings(p2m_engine* e, int slot, float* ms4) {
-    if (!e || !ms4 || slot < 0 || slot >= (int)e->slots.size()) { set_err("p2m_last_timings: bad argument"); return P2M_ERR_INVALID; }
+P2M_API int p2m_last_timings(p2m_engine* e, int slot, float* ms) {
+    if (!e || !ms || slot < 0 || slot >= (int)e->slots.size()) { set_err("p2m_last_timings: bad argument"); return P2M_ERR_INVALID; }
     Slot& s = *e->slots[slot];
-    double acc[4] = {0, 0, 0, 0};
+    double acc[Slot::kEv] = {0};
     CK(cudaSetDevice(s.dev));
     for (int r = 0; r < s.recorded; ++r) {
-        cudaEvent_t* ev = &s.ev[4 * r];
-        CK(cudaEventSynchronize(ev[3]));
+        cudaEvent_t* ev = &s.ev[Slot::kEv * r];
+        CK(cudaEventSynchronize(ev[Slot::kEv - 1]));
         float m;
-        CK(cudaEventElapsedTime(&m, ev[0], ev[1])); acc[0] += m;
-        CK(cudaEventElapsedTime(&m, ev[1], ev[2])); acc[1] += m;
-        CK(cudaEventElapsedTime(&m, ev[2], ev[3])); acc[2] += m;
-        CK(cudaEventElapsedTime(&m, ev[0], ev[3])); acc[3] += m;
+        for (int k = 0; k + 1 < Slot::kEv; ++k) { CK(cudaEventElapsedTime(&m, ev[k], ev[k + 1])); acc[k] += m; }
+        CK(cudaEventElapsedTime(&m, ev[0], ev[Slot::kEv - 1])); acc[Slot::kEv - 1] += m;
     }
-    for (int k = 0; k < 4; ++k) ms4[k] = s.recorded ? (float)(acc[k] / s.recorded) : 0.0f;
+    for (int k = 0; k < Slot::kEv; ++k) ms[k] = s.recorded ? (float)(acc[k] / s.recorded) : 0.0f;
     s.recorded = 0;
+    return P2M_OK;
+}
+
+P2M_API int p2m_set_scan_mode(p2m_engine* e, int mode) {
+    if (!e) { set_err("engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (mode != P2M_SCAN_GROUPED && mode != P2M_SCAN_FUSED) { set_err("p2m_set_scan_mode: unknown mode"); return P2M_ERR_INVALID; }
+    e->scan_mode = mode;
     return P2M_OK;
 }
 

@@ -1,0 +1,407 @@
+// p2m_grouped.cu -- the site-grouped query pipeline (default scan mode).
+//
+// Why: on the benchmark configs almost all scan work sits in interception lists of thousands of
+// faces that hundreds of queries share (the auxiliary sites inside closed surfaces), so scanning
+// each list once per tile of queries from shared memory turns an L2-bound gather (32 B sphere per
+// query per candidate) into a broadcast-fed fp32/fp64 compute loop.
+//
+//   k_descend       nearest_site (REF/SPEC.md:482-487) per row in Morton order -> site key; rows
+//                   outside D or nearest to a sentinel are answered here by the exact BVH fallback
+//                   (REF/SPEC.md:491) and keyed n_sites so the regroup sort moves them to the end
+//   (CUB radix sort of (site key, row); stable -> Morton order kept inside a site group)
+//   k_scan_grouped  CTA = 256 consecutive rows of the site-sorted order.  For each run of rows that
+//                   share a site, the CTA stages the site's list 256 entries at a time (face id,
+//                   fp64 sphere, fp32 sphere) in shared memory; every member thread scans the staged
+//                   chunk IN LIST ORDER for its own query (query_distance, REF/SPEC.md:488-496), so
+//                   its d_min evolves exactly as in the sequential oracle and even the counters match.
+//
+// Pruning per candidate, two stages, both conservative:
+//   fp32: skip iff |q_f - c_f|^2 > ((r_up + dmin_up + delta) * (1 + 1e-6))^2, where delta bounds the
+//         fp32 rounding of coordinates (4*sqrt(3)*2^-24*M, M = max |coordinate| of D) plus 2 eps.
+//         Whenever it skips, the fp64 test below would also skip.
+//   fp64: the oracle's test, |q-c|^2 > (r + d_min + eps)^2, then the exact point-triangle kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cub/device/device_scan.cuh>
+
+#include "p2m_device.cuh"
+#include "p2m_kernels.cuh"
+#include "p2m_traverse.cuh"
+
+namespace p2m {
+namespace dev {
+
+namespace {
+
+constexpr int kTile = 256;
+
+template <bool kCounters>
+__global__ void __launch_bounds__(256) k_descend(Params p, const double* __restrict__ q_xyz,
+                                                 const uint32_t* __restrict__ rows, uint64_t n,
+                                                 uint32_t* __restrict__ site_key, Out o) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t visited = 0, fb = 0;
+    if (i < n) {
+        const uint32_t row = rows[i];
+        const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+        const NN nn = nearest_site(p, q);
+        visited = nn.visited;
+        const bool in_d = q.x >= p.dmin[0] && q.x <= p.dmax[0] && q.y >= p.dmin[1] && q.y <= p.dmax[1] &&
+                          q.z >= p.dmin[2] && q.z <= p.dmax[2];
+        uint32_t flags = in_d ? 0u : 2u;
+        o.site[row] = nn.id;
+        if (nn.sentinel || !in_d) {
+            flags |= 1u;
+            fb = 1;
+            double best;
+            const uint32_t bf = bvh_closest(p, q, &best);
+            V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+                 __longlong_as_double(0x7ff8000000000000ll)};
+            if (bf != 0xffffffffu) {
+                V a, b, c;
+                load_tri(p.rec + 4 * (uint64_t)bf, &a, &b, &c);
+                closest_tri(q, a, b, c, &cp);
+            }
+            o.dist[row] = sqrt(best);
+            o.cp[3 * (uint64_t)row] = cp.x;
+            o.cp[3 * (uint64_t)row + 1] = cp.y;
+            o.cp[3 * (uint64_t)row + 2] = cp.z;
+            o.face[row] = bf;
+            site_key[i] = p.n_nodes;  // sorts after every real site
+            if (kCounters && o.per_query) {
+                o.per_query[3 * (uint64_t)row] = 0;
+                o.per_query[3 * (uint64_t)row + 1] = 0;
+            }
+        } else {
+            site_key[i] = nn.id;
+        }
+        if (o.flags) o.flags[row] = flags;
+        if (kCounters && o.per_query) o.per_query[3 * (uint64_t)row + 2] = visited;
+    }
+    if (kCounters && o.agg) {
+        unsigned long long v0 = visited, v1 = fb;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            v0 += __shfl_down_sync(0xffffffffu, v0, s);
+            v1 += __shfl_down_sync(0xffffffffu, v1, s);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(o.agg + 2, v0);
+            atomicAdd(o.agg + 3, v1);
+        }
+    }
+}
+
+// ---- tile construction over the site-sorted order --------------------------------------------
+// tiles = maximal runs of equal site key cut every kTile rows; fallback rows (key == n_sites) are
+// excluded.  hpos[i] = i at a run head else 0 -> inclusive max-scan gives each row its run start.
+__global__ void __launch_bounds__(256) k_run_heads(const uint32_t* __restrict__ key, uint64_t n,
+                                                   uint32_t* __restrict__ hpos) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    hpos[i] = (i == 0 || key[i] != key[i - 1]) ? (uint32_t)i : 0u;
+}
+
+// Tile height: kTile rows, or p.long_tile rows for "heavy" sites (many exact evaluations expected
+// per query, p.heavy, estimated at engine creation), so replicas split their lists and a heavy
+// site spreads over more SMs.
+__global__ void __launch_bounds__(256) k_tile_flags(Params p, const uint32_t* __restrict__ key,
+                                                    const uint32_t* __restrict__ run_start, uint64_t n,
+                                                    uint32_t n_sites, uint32_t* __restrict__ flag,
+                                                    uint32_t* __restrict__ meta) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = key[i];
+    const uint32_t rs = run_start[i];
+    uint32_t T = kTile;
+    if (k < n_sites && p.heavy[k]) T = p.long_tile;
+    flag[i] = (k < n_sites && ((uint32_t)i == rs || (((uint32_t)i - rs) % T) == 0)) ? 1u : 0u;
+    // number of table rows (fallback rows sort last)
+    const bool last_valid = k < n_sites && (i + 1 == n || key[i + 1] >= n_sites);
+    if (last_valid) meta[1] = (uint32_t)(i + 1);
+    if (i == 0 && k >= n_sites) meta[1] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_tile_write(const uint32_t* __restrict__ flag,
+                                                    const uint32_t* __restrict__ tix, uint64_t n,
+                                                    uint32_t* __restrict__ tiles, uint32_t* __restrict__ meta) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (flag[i]) tiles[tix[i]] = (uint32_t)i;
+    if (i + 1 == n) meta[0] = tix[i] + flag[i];
+}
+
+// ---- the tile scan --------------------------------------------------------------------------
+// packed fp32 pairs (sm_100a f32x2): two candidates per instruction in the pre-filter
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2_up(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rp.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2_up(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rp.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+// One CTA per tile (all rows share one site).  A tile of m rows uses G = ceil(m/32) warps per
+// replica and R = 8 / G replicas; replica r scans the 32-candidate batches b == r (mod R) of every
+// staged chunk, so small groups still keep all 8 warps busy.  Per batch, each lane computes a
+// pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
+// warp walks the union of set bits in list order; a lane whose bit is set applies the oracle's fp64
+// sphere test with its CURRENT d_min and, on pass, the exact point-triangle kernel on the triangle
+// staged in shared memory (all lanes read the same record: broadcast).  Because the pre-filter can
+// only skip candidates the fp64 test would skip, each replica evaluates exactly the candidates the
+// sequential oracle would (so with R = 1 the counters match the oracle too).  Replicas are merged by
+// the lexicographic min of (d^2, face id), the sequential argmin.
+constexpr int kChunk = 256;
+constexpr int kWarps = kTile / 32;
+
+template <bool kCounters>
+__global__ void __launch_bounds__(kTile, 2) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
+                                                         const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ key,
+                                                         const uint32_t* __restrict__ tiles,
+                                                         const uint32_t* __restrict__ meta, Out o) {
+    __shared__ D4 s_rec[kChunk * 4];            // 128-byte face records (sphere, triangle)
+    __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
+    __shared__ uint32_t s_fid[kChunk];
+    __shared__ double s_rd[kTile];
+    __shared__ uint32_t s_rf[kTile];
+    __shared__ uint32_t s_re[kTile];
+    const uint32_t nt = meta[0];
+    const uint32_t b = blockIdx.x;
+    if (b >= nt) return;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t start = tiles[b];
+    const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
+    const int m = (int)(stop - start);
+    const uint32_t s = key[start];
+    const int G = (m + 31) >> 5;
+    const int R = max(1, kWarps / G);
+    const int r = w / G;                         // replica of this warp (uniform per warp)
+    const int j = (w % G) * 32 + lane;
+    const bool warp_on = r < R;
+    const bool active = warp_on && j < m;
+    uint32_t row = 0;
+    V q{0, 0, 0};
+    uint64_t QX = 0, QY = 0, QZ = 0;
+    if (active) {
+        row = rows[start + j];
+        q = V{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+        const float fx = (float)q.x, fy = (float)q.y, fz = (float)q.z;
+        QX = pk2(fx, fx); QY = pk2(fy, fy); QZ = pk2(fz, fz);
+    }
+    const float K = 1.000001f;
+    const float delta = p.f32_delta;
+    const float finf = __int_as_float(0x7f800000);
+    double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
+    uint64_t DK = pk2(finf, finf);               // (dmin_up + delta) * K, rounded up, both halves
+    uint32_t bf = 0xffffffffu;
+    uint32_t exact = 0;
+    const uint64_t beg = p.off[s], end = p.off[s + 1];
+    float* s_pf = reinterpret_cast<float*>(s_pair);
+    for (uint64_t base = beg; base < end; base += kChunk) {
+        const int mc = (int)min((uint64_t)kChunk, end - base);
+        if (base != beg) __syncthreads();
+        for (int t = tid; t < ((mc + 1) & ~1); t += kTile) {
+            const int pp = t >> 1, h = t & 1;
+            if (t < mc) {
+                const uint32_t f = p.lf[base + t];
+                const D4* rec = p.rec + 4 * (uint64_t)f;
+                const D4 sp = ldg4(rec);
+                s_rec[4 * t] = sp;
+                s_rec[4 * t + 1] = ldg4(rec + 1);
+                s_rec[4 * t + 2] = ldg4(rec + 2);
+                s_rec[4 * t + 3] = ldg4(rec + 3);
+                s_fid[t] = f;
+                s_pf[8 * pp + h] = (float)sp.x;
+                s_pf[8 * pp + 2 + h] = (float)sp.y;
+                s_pf[8 * pp + 4 + h] = (float)sp.z;
+                s_pf[8 * pp + 6 + h] = __fmul_ru(__double2float_ru(sp.w), K);
+            } else {  // odd tail: a never-passing dummy (masked out below anyway)
+                s_pf[8 * pp + h] = finf; s_pf[8 * pp + 2 + h] = 0.f; s_pf[8 * pp + 4 + h] = 0.f; s_pf[8 * pp + 6 + h] = 0.f;
+            }
+        }
+        __syncthreads();
+        if (!warp_on) continue;
+        const int nb = (mc + 31) >> 5;
+        for (int bb = r; bb < nb; bb += R) {
+            const int k0 = bb * 32;
+            uint32_t mask = 0;
+            if (active) {
+#pragma unroll
+                for (int pp = 0; pp < 16; ++pp) {
+                    const float4 A = s_pair[k0 + 2 * pp], B = s_pair[k0 + 2 * pp + 1];
+                    const uint64_t dx = sub2(QX, pk2(A.x, A.y));
+                    const uint64_t dy = sub2(QY, pk2(A.z, A.w));
+                    const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
+                    const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+                    const uint64_t th = add2_up(pk2(B.z, B.w), DK);
+                    const uint64_t t2 = mul2_up(th, th);
+                    float d0, d1, t0, t1;
+                    upk2(d2, d0, d1);
+                    upk2(t2, t0, t1);
+                    mask |= (uint32_t)(!(d0 > t0)) << (2 * pp);
+                    mask |= (uint32_t)(!(d1 > t1)) << (2 * pp + 1);
+                }
+                const int valid = mc - k0;
+                if (valid < 32) mask &= (1u << valid) - 1u;
+            }
+            uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+            while (um) {
+                const int kk = __ffs(um) - 1;
+                um &= um - 1;
+                if ((mask >> kk) & 1u) {
+                    const int k = k0 + kk;
+                    const D4 sp = s_rec[4 * k];
+                    const double dc2 = vd2(q, V{sp.x, sp.y, sp.z});
+                    const double t = sp.w + dmin + p.prune_eps;
+                    if (!(dc2 > t * t)) {
+                        const D4 t0 = s_rec[4 * k + 1], t1 = s_rec[4 * k + 2], t2 = s_rec[4 * k + 3];
+                        V pp3;
+                        const double dd = closest_tri(q, V{t0.x, t0.y, t0.z}, V{t0.w, t1.x, t1.y}, V{t1.z, t1.w, t2.x}, &pp3);
+                        ++exact;
+                        const uint32_t f = s_fid[k];
+                        if (dd < best || (dd == best && f < bf)) {
+                            best = dd;
+                            bf = f;
+                            dmin = sqrt(dd);
+                            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+                            DK = pk2(dkf, dkf);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (R > 1) {
+        __syncthreads();
+        const int slot = r * G * 32 + j;
+        if (active) { s_rd[slot] = best; s_rf[slot] = bf; s_re[slot] = exact; }
+        __syncthreads();
+        if (active && r == 0) {
+            for (int rr = 1; rr < R; ++rr) {
+                const int o2 = rr * G * 32 + j;
+                const double d2 = s_rd[o2];
+                const uint32_t f2 = s_rf[o2];
+                if (d2 < best || (d2 == best && f2 < bf)) { best = d2; bf = f2; }
+                exact += s_re[o2];
+            }
+        }
+    }
+    const bool writer = active && r == 0;
+    if (writer) {
+        V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+             __longlong_as_double(0x7ff8000000000000ll)};
+        if (bf != 0xffffffffu) {
+            V a, bb, c;
+            load_tri(p.rec + 4 * (uint64_t)bf, &a, &bb, &c);
+            closest_tri(q, a, bb, c, &cp);
+        }
+        o.dist[row] = sqrt(best);
+        o.cp[3 * (uint64_t)row] = cp.x;
+        o.cp[3 * (uint64_t)row + 1] = cp.y;
+        o.cp[3 * (uint64_t)row + 2] = cp.z;
+        o.face[row] = bf;
+        if (kCounters && o.per_query) {
+            o.per_query[3 * (uint64_t)row] = end - beg;
+            o.per_query[3 * (uint64_t)row + 1] = exact;
+        }
+    }
+    if (kCounters && o.agg) {
+        unsigned long long v0 = writer ? (end - beg) : 0ull, v1 = writer ? exact : 0u;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            v0 += __shfl_down_sync(0xffffffffu, v0, sh);
+            v1 += __shfl_down_sync(0xffffffffu, v1, sh);
+        }
+        if (lane == 0) {
+            atomicAdd(o.agg + 0, v0);
+            atomicAdd(o.agg + 1, v1);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_descend(const Params& p, const double* q, const uint32_t* rows, uint64_t n, uint32_t* site_key,
+                           const Out& o, bool counters, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (counters) k_descend<true><<<g, 256, 0, s>>>(p, q, rows, n, site_key, o);
+    else k_descend<false><<<g, 256, 0, s>>>(p, q, rows, n, site_key, o);
+    return cudaGetLastError();
+}
+
+struct MaxU32 {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+static cudaError_t scan_max_u32(void* tmp, size_t bytes, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+    return cub::DeviceScan::InclusiveScan(tmp, bytes, in, out, MaxU32{}, (int64_t)n, s);
+}
+static cudaError_t scan_sum_u32(void* tmp, size_t bytes, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+    return cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int64_t)n, s);
+}
+
+size_t tiles_tmp_bytes(uint64_t n) {
+    size_t a = 0, b = 0;
+    scan_max_u32(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr, n, 0);
+    scan_sum_u32(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, n, 0);
+    return std::max(a, b);
+}
+
+cudaError_t launch_tiles(const Params& p, const uint32_t* key, uint64_t n, uint32_t n_sites, uint32_t* hpos, uint32_t* run_start,
+                         uint32_t* flag, uint32_t* tix, uint32_t* tiles, uint32_t* meta, void* tmp, size_t tmp_bytes,
+                         cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    cudaError_t e;
+    k_run_heads<<<g, 256, 0, s>>>(key, n, hpos);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = scan_max_u32(tmp, tmp_bytes, hpos, run_start, n, s)) != cudaSuccess) return e;
+    k_tile_flags<<<g, 256, 0, s>>>(p, key, run_start, n, n_sites, flag, meta);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = scan_sum_u32(tmp, tmp_bytes, flag, tix, n, s)) != cudaSuccess) return e;
+    k_tile_write<<<g, 256, 0, s>>>(flag, tix, n, tiles, meta);
+    return cudaGetLastError();
+}
+
+uint64_t max_tiles(uint64_t n, uint64_t n_sites) { return std::min<uint64_t>(n, n_sites) + (n + 31) / 32 + 1; }
+
+cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* rows, const uint32_t* key,
+                              const uint32_t* tiles, const uint32_t* meta, uint64_t n, const Out& o, bool counters,
+                              cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const unsigned g = (unsigned)max_tiles(n, p.n_nodes);
+    if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, o);
+    else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, o);
+    return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace p2m
