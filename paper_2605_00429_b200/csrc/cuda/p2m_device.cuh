@@ -87,6 +87,7 @@ struct Params {
     const D4* kd;           // S nodes
     uint32_t n_nodes;
     const D4* rec;          // 4 per face
+    const float4* f32;      // per face fp32 pre-filter record: c rounded to nearest, r_up * K rounded up
     const uint64_t* off;    // S+1
     const uint32_t* lf;     // list entries
     const D4* bvh;          // 2 per node

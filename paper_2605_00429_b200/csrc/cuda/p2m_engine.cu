@@ -152,6 +152,7 @@ struct Slot {
     int dev = 0;
     cudaStream_t stream = nullptr;
     D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
+    float4* f32 = nullptr;
     uint64_t* off = nullptr;
     uint32_t *lf = nullptr, *bvh_perm = nullptr;
     uint8_t* heavy = nullptr;
@@ -186,6 +187,7 @@ void free_slot(Slot& s) {
     cudaSetDevice(s.dev);
     cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
     cudaFree(s.heavy);
+    cudaFree(s.f32);
     cudaFree(s.q); cudaFree(s.dist); cudaFree(s.cp); cudaFree(s.face); cudaFree(s.site); cudaFree(s.flags);
     cudaFree(s.agg);
     for (auto& e : s.ev) if (e) cudaEventDestroy(e);
@@ -198,6 +200,7 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
     CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
@@ -389,6 +392,18 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         rec[4 * f + 2] = D4{t[4], t[5], t[6], t[7]};
         rec[4 * f + 3] = D4{t[8], 0.0, 0.0, 0.0};
     }
+    // fp32 pre-filter records (k_scan_tiles): centre rounded to nearest, radius rounded up and
+    // multiplied by K = 1.000001 rounding up -- the same values the kernel's bound assumes
+    std::vector<float4> f32(F);
+    for (uint64_t f = 0; f < F; ++f) {
+        const double* sp = d->face_sphere + 4 * f;
+        float r = (float)sp[3];
+        if ((double)r < sp[3]) r = std::nextafter(r, INFINITY);
+        const double prod = (double)r * (double)1.000001f;
+        float rk = (float)prod;
+        if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
+        f32[f] = make_float4((float)sp[0], (float)sp[1], (float)sp[2], rk);
+    }
     FlatBvh bvh;
     build_bvh(d->tri_xyz, F, bvh);
     E->n_bvh = bvh.nodes.size() / 2;
@@ -445,6 +460,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         cudaSetDevice(s0.dev);
         if (cudaMemcpy(s0.kd, kd.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.rec, rec.data(), sizeof(D4) * 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.f32, f32.data(), sizeof(float4) * F, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
             cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -453,7 +469,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             return fail(P2M_ERR_CUDA);
         }
     }
-    E->bytes = sizeof(D4) * (S + 4 * F + bvh.nodes.size()) + 8 * (S + 1) + 4 * (L + F);
+    E->bytes = sizeof(D4) * (S + 4 * F + bvh.nodes.size()) + sizeof(float4) * F + 8 * (S + 1) + 4 * (L + F) + S;
     auto t0 = std::chrono::steady_clock::now();
     for (size_t k = 1; k < E->slots.size(); ++k) {
         Slot& s = *E->slots[k];
@@ -468,7 +484,8 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             }
         }
         struct { void* dst; const void* src; size_t n; } cp[] = {
-            {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.off, s0.off, 8 * (S + 1)},
+            {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
+            {s.off, s0.off, 8 * (S + 1)},
             {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F}};
         for (auto& c : cp)
             if (c.n && cudaMemcpyPeerAsync(c.dst, s.dev, c.src, s0.dev, c.n, s.stream) != cudaSuccess) {
@@ -483,7 +500,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto& s : E->slots) {
         s->params = P;
-        s->params.kd = s->kd; s->params.rec = s->rec; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.off = s->off; s->params.lf = s->lf;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
     }
     {

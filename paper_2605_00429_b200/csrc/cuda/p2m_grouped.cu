@@ -182,12 +182,11 @@ constexpr int kChunk = 256;
 constexpr int kWarps = kTile / 32;
 
 template <bool kCounters>
-__global__ void __launch_bounds__(kTile, 2) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
+__global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
                                                          const uint32_t* __restrict__ rows,
                                                          const uint32_t* __restrict__ key,
                                                          const uint32_t* __restrict__ tiles,
                                                          const uint32_t* __restrict__ meta, Out o) {
-    __shared__ D4 s_rec[kChunk * 4];            // 128-byte face records (sphere, triangle)
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
     __shared__ double s_rd[kTile];
@@ -225,29 +224,26 @@ __global__ void __launch_bounds__(kTile, 2) k_scan_tiles(Params p, const double*
     uint32_t exact = 0;
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     float* s_pf = reinterpret_cast<float*>(s_pair);
+    // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
+    uint32_t nf = 0;
+    float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
+    if (beg + tid < end) { nf = p.lf[beg + tid]; nv = p.f32[nf]; }
     for (uint64_t base = beg; base < end; base += kChunk) {
         const int mc = (int)min((uint64_t)kChunk, end - base);
-        if (base != beg) __syncthreads();
-        for (int t = tid; t < ((mc + 1) & ~1); t += kTile) {
-            const int pp = t >> 1, h = t & 1;
-            if (t < mc) {
-                const uint32_t f = p.lf[base + t];
-                const D4* rec = p.rec + 4 * (uint64_t)f;
-                const D4 sp = ldg4(rec);
-                s_rec[4 * t] = sp;
-                s_rec[4 * t + 1] = ldg4(rec + 1);
-                s_rec[4 * t + 2] = ldg4(rec + 2);
-                s_rec[4 * t + 3] = ldg4(rec + 3);
-                s_fid[t] = f;
-                s_pf[8 * pp + h] = (float)sp.x;
-                s_pf[8 * pp + 2 + h] = (float)sp.y;
-                s_pf[8 * pp + 4 + h] = (float)sp.z;
-                s_pf[8 * pp + 6 + h] = __fmul_ru(__double2float_ru(sp.w), K);
-            } else {  // odd tail: a never-passing dummy (masked out below anyway)
-                s_pf[8 * pp + h] = finf; s_pf[8 * pp + 2 + h] = 0.f; s_pf[8 * pp + 4 + h] = 0.f; s_pf[8 * pp + 6 + h] = 0.f;
-            }
+        if (base != beg) __syncthreads();        // the previous chunk is fully consumed
+        {
+            const int pp = tid >> 1, h = tid & 1;
+            if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
+            s_fid[tid] = nf;
+            s_pf[8 * pp + h] = nv.x;
+            s_pf[8 * pp + 2 + h] = nv.y;
+            s_pf[8 * pp + 4 + h] = nv.z;
+            s_pf[8 * pp + 6 + h] = nv.w;
         }
         __syncthreads();
+        // prefetch the next chunk while this one is scanned
+        const uint64_t nxt = base + kChunk + tid;
+        if (nxt < end) { nf = p.lf[nxt]; nv = p.f32[nf]; }
         if (!warp_on) continue;
         const int nb = (mc + 31) >> 5;
         for (int bb = r; bb < nb; bb += R) {
@@ -277,16 +273,16 @@ __global__ void __launch_bounds__(kTile, 2) k_scan_tiles(Params p, const double*
                 const int kk = __ffs(um) - 1;
                 um &= um - 1;
                 if ((mask >> kk) & 1u) {
-                    const int k = k0 + kk;
-                    const D4 sp = s_rec[4 * k];
+                    const uint32_t f = s_fid[k0 + kk];
+                    const D4* rec = p.rec + 4 * (uint64_t)f;   // same address across the warp
+                    const D4 sp = ldg4(rec);
                     const double dc2 = vd2(q, V{sp.x, sp.y, sp.z});
                     const double t = sp.w + dmin + p.prune_eps;
                     if (!(dc2 > t * t)) {
-                        const D4 t0 = s_rec[4 * k + 1], t1 = s_rec[4 * k + 2], t2 = s_rec[4 * k + 3];
-                        V pp3;
-                        const double dd = closest_tri(q, V{t0.x, t0.y, t0.z}, V{t0.w, t1.x, t1.y}, V{t1.z, t1.w, t2.x}, &pp3);
+                        V a, bb3, c3, pp3;
+                        load_tri(rec, &a, &bb3, &c3);
+                        const double dd = closest_tri(q, a, bb3, c3, &pp3);
                         ++exact;
-                        const uint32_t f = s_fid[k];
                         if (dd < best || (dd == best && f < bf)) {
                             best = dd;
                             bf = f;

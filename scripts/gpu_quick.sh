@@ -1,9 +1,8 @@
-set -x
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
-python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -15
-for m in 0 1; do python bench.py --steps 5 --warmup 3 --scan-mode $m --no-cpu-baseline > gpurun_out/bench_m$m.json 2> gpurun_out/bench_m$m.err; echo rc=$?; tail -3 gpurun_out/bench_m$m.err; done
-python bench.py --steps 5 --warmup 3 --config 1 --no-cpu-baseline > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
-cat gpurun_out/bench_m0.json gpurun_out/bench_c1.json | python -c "
-import json,sys
-for l in sys.stdin:
-    d=json.loads(l); print(d['value']/1e6, 'Mq/s', d['config']['split_ms'], 'frac', d['roofline']['frac'], 'e2e', d['e2e']['value']/1e6)"
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
+for cfg in 1 2; do
+python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/q_$cfg.json 2>gpurun_out/q_$cfg.err
+python -c "
+import json; d=json.load(open('gpurun_out/q_$cfg.json')); s=d['config']['split_ms']
+print('c$cfg', round(d['value']/1e6,1), 'Mq/s', {k: round(v,2) for k,v in s.items()}, 'exact/q', round(d['config']['per_query']['exact'],1), 'frac', round(d['roofline']['frac'],2))"
+done
