@@ -114,7 +114,10 @@ def build_workload(cfg, rank, world, n_per_rank, build_threads, aux_corner_union
     h = P.HostEngine.build(V, F, P.BuildConfig(n_threads=build_threads, aux_corner_union=aux_corner_union))
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
-    q = P.gen_queries(cfg, V, F, rank * n_per_rank, n_per_rank)
+    from paper_2605_00429_b200 import shard
+
+    first, count = shard.rank_slice(rank, world, n_per_rank)
+    q = P.gen_queries(cfg, V, F, first, count)
     t_q = time.perf_counter() - t0
     return V, F, h, q, {"mesh_s": round(t_mesh, 3), "build_s": round(t_build, 3), "queries_s": round(t_q, 3)}
 
@@ -202,6 +205,7 @@ def main():
 
     import paper_2605_00429_b200 as P
     from paper_2605_00429_b200 import _lib as L
+    from paper_2605_00429_b200 import shard
 
     if world > 1:
         torch.cuda.set_device(local)
@@ -265,10 +269,7 @@ def main():
     L.check(lib.p2m_last_timings(eng.handle, 0, split))
     L.check(lib.p2m_set_profiling(eng.handle, 0))
     split = [float(x) for x in split]
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ms_max = shard.max_over_ranks(ms, dist if world > 1 else None)
     value = n * world / (ms_max / 1e3)
 
     # e2e: the public host-buffer API (p2m_query) with pinned host memory, H2D + D2H inside
@@ -292,10 +293,7 @@ def main():
     for _ in range(args.e2e_steps):
         e2e_call()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    t_e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-    e2e_value = n * world / float(t_e.item())
+    e2e_value = n * world / shard.max_over_ranks(e2e_s, dist if world > 1 else None)
     # the e2e rows must equal the device-resident rows (same engine, same inputs)
     same = bool(torch.equal(o_dist, ddist.cpu()) and torch.equal(o_face, dface.cpu()))
 

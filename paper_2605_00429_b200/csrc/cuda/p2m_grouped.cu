@@ -357,10 +357,10 @@ cudaError_t launch_descend(const Params& p, const double* q, const uint32_t* row
 struct MaxU32 {
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
 };
-static cudaError_t scan_max_u32(void* tmp, size_t bytes, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+static cudaError_t scan_max_u32(void* tmp, size_t& bytes, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
     return cub::DeviceScan::InclusiveScan(tmp, bytes, in, out, MaxU32{}, (int64_t)n, s);
 }
-static cudaError_t scan_sum_u32(void* tmp, size_t bytes, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+static cudaError_t scan_sum_u32(void* tmp, size_t& bytes, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
     return cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, (int64_t)n, s);
 }
 
@@ -379,10 +379,12 @@ cudaError_t launch_tiles(const Params& p, const uint32_t* key, uint64_t n, uint3
     cudaError_t e;
     k_run_heads<<<g, 256, 0, s>>>(key, n, hpos);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = scan_max_u32(tmp, tmp_bytes, hpos, run_start, n, s)) != cudaSuccess) return e;
+    size_t tb = tmp_bytes;
+    if ((e = scan_max_u32(tmp, tb, hpos, run_start, n, s)) != cudaSuccess) return e;
     k_tile_flags<<<g, 256, 0, s>>>(p, key, run_start, n, n_sites, flag, meta);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = scan_sum_u32(tmp, tmp_bytes, flag, tix, n, s)) != cudaSuccess) return e;
+    tb = tmp_bytes;
+    if ((e = scan_sum_u32(tmp, tb, flag, tix, n, s)) != cudaSuccess) return e;
     k_tile_write<<<g, 256, 0, s>>>(flag, tix, n, tiles, meta);
     return cudaGetLastError();
 }

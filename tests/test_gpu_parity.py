@@ -1,15 +1,23 @@
 """GPU parity: the CUDA query path (through the C ABI) vs the CPU oracle on identical inputs.
 
 Bar (BASELINE.json north_star): site and face ids exact, distance and closest point within 1e-6
-relative.  fp64 with --fmad=false and the reference's operation order makes the whole row
-bit-identical, which is what these tests assert (tolerance 0)."""
+relative.  fp64 with --fmad=false and the reference's operation order makes every row
+bit-identical, which is what these tests assert (tolerance 0, stricter than 1e-6 relative).
+Edge cases follow the SPEC's examples: empty batch (REF/SPEC.md:503), duplicated point (504),
+q = mesh vertex (494), out-of-domain rows answered by the fallback (491, 611), tiny meshes."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
 import oracle as O
 import paper_2605_00429_b200 as P
+from paper_2605_00429_b200 import _lib as L
 
 pytestmark = pytest.mark.gpu
+
+TET_V = np.array([[1.0, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]])
+TET_F = np.array([[0, 1, 2], [0, 3, 1], [0, 2, 3], [1, 3, 2]], np.uint32)
 
 
 def _compare(r, ref, n):
@@ -19,10 +27,23 @@ def _compare(r, ref, n):
         assert len(bad) == 0, f"{k}: {len(bad)} of {n} rows differ, first {bad[:5]}"
     for k in ("distance", "closest"):
         a, b = getattr(r, k), ref[k]
-        assert a.tobytes() == b.tobytes(), f"{k} not bit-identical (max rel {np.nanmax(np.abs(a-b)/np.maximum(np.abs(b),1e-300))})"
+        assert a.tobytes() == b.tobytes(), f"{k} not bit-identical"
 
 
-@pytest.mark.parametrize("fixture,nq,cfg", [("ico3", 20000, None), ("c1", 200000, 1), ("c2", 200000, 2)])
+def _check_counters(r, ref, sequential):
+    c, rc = r.counters, ref["counters"]
+    # candidates (= list length of the nearest site, REF/SPEC.md:511) are deterministic
+    assert c["candidates_visited"] == rc["candidates_visited"]
+    assert c["fallbacks"] == rc["fallbacks"]
+    assert c["exact_evaluations"] + c["pruned"] == c["candidates_visited"]  # REF/SPEC.md:511
+    # the stack-free descent visits exactly the oracle's nodes, in the oracle's order
+    assert c["kd_nodes_visited"] == rc["kd_nodes_visited"]
+    if sequential:
+        # the fused per-row path also scans the list in the oracle's order: all counters match
+        assert c["exact_evaluations"] == rc["exact_evaluations"]
+
+
+@pytest.mark.parametrize("fixture,nq,cfg", [("ico3", 20000, None), ("c1", 300000, 1), ("c2", 300000, 2)])
 def test_parity_vs_oracle(request, fixture, nq, cfg):
     V, F, h = request.getfixturevalue(fixture)
     if cfg is None:
@@ -33,20 +54,12 @@ def test_parity_vs_oracle(request, fixture, nq, cfg):
     r = eng.batch_query(q)
     ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
     _compare(r, ref, nq)
-    # counters: candidates (= list length of the nearest site) and k-d nodes visited are deterministic
-    # (REF/SPEC.md:511); exact evaluations depend on the pruning order (replicas split small groups)
-    c, rc = r.counters, ref["counters"]
-    assert c["candidates_visited"] == rc["candidates_visited"]
-    assert c["kd_nodes_visited"] == rc["kd_nodes_visited"]
-    assert c["fallbacks"] == rc["fallbacks"]
-    assert c["exact_evaluations"] + c["pruned"] == c["candidates_visited"]
+    _check_counters(r, ref, sequential=False)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
 def test_scan_modes_identical(c2, mode):
-    """Grouped (site-tiled, shared-memory) and fused (per-row) scans give the same rows and counters."""
-    import ctypes as C
-    from paper_2605_00429_b200 import _lib as L
+    """Grouped (site tiles, shared memory) and fused (one thread per row) scans give the same rows."""
     V, F, h = c2
     q = P.gen_queries(2, V, F, 500_000, 100_000)
     eng = P.Engine(h)
@@ -54,6 +67,137 @@ def test_scan_modes_identical(c2, mode):
     r = eng.batch_query(q)
     ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
     _compare(r, ref, len(q))
-    assert r.counters["candidates_visited"] == ref["counters"]["candidates_visited"]
-    if mode == 1:  # the fused per-row scan prunes in list order exactly like the oracle
-        assert r.counters["exact_evaluations"] == ref["counters"]["exact_evaluations"]
+    _check_counters(r, ref, sequential=(mode == 1))
+
+
+def test_golden_engine_on_gpu():
+    """The committed reference-generated fixture (tests/golden/engine_ico2.npz) on the GPU."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "engine_ico2.npz"))
+    h = P.HostEngine.build(g["vertices"], g["faces"])
+    a = h.arrays()
+    assert a["list_faces"].tobytes() == g["list_faces"].tobytes()  # same build on this box
+    r = P.Engine(h).batch_query(g["q"])
+    for k in ("distance", "closest", "face", "site", "flags"):
+        assert getattr(r, k).tobytes() == g[k].tobytes(), k
+
+
+def test_empty_and_duplicated_batches(ico3):
+    V, F, h = ico3
+    eng = P.Engine(h)
+    r = eng.batch_query(np.zeros((0, 3)))
+    assert len(r.distance) == 0 and all(v == 0 for v in r.counters.values())  # REF/SPEC.md:503
+    for mode in (0, 1):
+        L.check(L.cuda().p2m_set_scan_mode(eng.handle, mode))
+        one = eng.batch_query(np.array([[0.3, -0.2, 0.5]]))
+        many = eng.batch_query(np.tile([[0.3, -0.2, 0.5]], (1000, 1)))
+        assert np.all(many.distance == one.distance[0]) and np.all(many.face == one.face[0])
+        # REF/SPEC.md:504; exact evaluations depend on how the grouped scan splits a tile (a lone row
+        # gets 8 replicas), so that counter is checked on the sequential fused path only
+        keys = ("candidates_visited", "kd_nodes_visited") + (("exact_evaluations",) if mode == 1 else ())
+        for k in keys:
+            assert many.counters[k] == 1000 * one.counters[k], (mode, k)
+
+
+def test_vertex_queries_and_out_of_domain(ico3):
+    V, F, h = ico3
+    eng = P.Engine(h)
+    r = eng.batch_query(V)
+    assert np.all(r.distance == 0.0)  # REF/SPEC.md:494
+    for i in range(0, len(V), 17):
+        assert i in F[r.face[i]]
+    a = h.arrays()
+    far = np.array([[100.0, 0, 0], [0, -250.0, 3.0], [1e6, 1e6, 1e6], [a["domain"][3] + 1e-9, 0, 0]])
+    r = eng.batch_query(far)
+    assert np.all((r.flags & 3) == 3) and r.counters["fallbacks"] == len(far)
+    tri = a["tri"].reshape(-1, 9)
+    for i, q in enumerate(far):
+        d2, p, f = O.brute_force_closest(tri, q)
+        assert r.face[i] == f and r.distance[i] == np.sqrt(d2) and r.closest[i].tobytes() == p.tobytes()
+
+
+@pytest.mark.parametrize("mesh", ["tri", "tet"])
+def test_tiny_meshes(mesh):
+    V, F = {"tri": (np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0]]), np.array([[0, 1, 2]], np.uint32)),
+            "tet": (TET_V, TET_F)}[mesh]
+    h = P.HostEngine.build(V, F)
+    q = np.random.default_rng(1).uniform(-3, 3, size=(5000, 3))
+    r = P.Engine(h).batch_query(q)
+    ref = O.OracleEngine(h.arrays()).batch_query(q)
+    _compare(r, ref, len(q))
+
+
+def test_nearest_site_and_per_query_counters(c1):
+    import torch
+    V, F, h = c1
+    q = P.gen_queries(1, V, F, 0, 50_000)
+    eng = P.Engine(h)
+    dq = torch.from_numpy(q).cuda()
+    site = torch.empty(len(q), dtype=torch.int32, device="cuda")
+    pq = torch.empty((len(q), 3), dtype=torch.int64, device="cuda")
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    L.check(L.cuda().p2m_nearest_site_device(eng.handle, 0, C.c_void_p(dq.data_ptr()), len(q),
+                                             C.c_void_p(site.data_ptr()), s))
+    L.check(L.cuda().p2m_query_device_counters(eng.handle, 0, C.c_void_p(dq.data_ptr()), len(q),
+                                               C.c_void_p(pq.data_ptr()), s))
+    torch.cuda.synchronize()
+    ref = O.OracleEngine(h.arrays()).batch_query(q, per_query=True)
+    assert np.array_equal(site.cpu().numpy().astype(np.uint32), ref["site"])
+    pq = pq.cpu().numpy()
+    assert np.array_equal(pq[:, 0], ref["per_query"][:, 0])
+    assert np.array_equal(pq[:, 2], ref["per_query"][:, 2])
+
+
+def test_multi_slot_engine_shards_and_replicates(c2):
+    """Two replicas on device 0 exercise the peer-replica copy and the per-device host threads of
+    p2m_query on a single GPU; rows must not depend on the shard they land in."""
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 0, 200_001)
+    r1 = P.Engine(h, devices=[0]).batch_query(q)
+    e2 = P.Engine(h, devices=[0, 0])
+    assert e2.info()["n_devices"] == 2
+    r2 = e2.batch_query(q)
+    for k in ("distance", "closest", "face", "site", "flags"):
+        assert getattr(r1, k).tobytes() == getattr(r2, k).tobytes(), k
+    assert r1.counters["candidates_visited"] == r2.counters["candidates_visited"]
+
+
+def test_device_api_on_torch_stream(c2):
+    """p2m_query_device on caller-owned device buffers and stream == the host-buffer API."""
+    import torch
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 7, 123_457)
+    eng = P.Engine(h)
+    n = len(q)
+    dq = torch.from_numpy(q).cuda()
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty((n, 3), dtype=torch.float64, device="cuda")] + \
+           [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        L.check(L.cuda().p2m_query_device(eng.handle, 0, C.c_void_p(dq.data_ptr()), n,
+                                          *[C.c_void_p(t.data_ptr()) for t in outs],
+                                          C.c_void_p(st.cuda_stream), None))
+    st.synchronize()
+    r = eng.batch_query(q)
+    assert outs[0].cpu().numpy().tobytes() == r.distance.tobytes()
+    assert np.array_equal(outs[2].cpu().numpy().astype(np.uint32), r.face)
+
+
+def test_kernel_launch_count(ico3):
+    V, F, h = ico3
+    eng = P.Engine(h)
+    n = C.c_int()
+    L.check(L.cuda().p2m_kernels_per_query(eng.handle, 100000, C.byref(n)))
+    assert 6 <= n.value <= 30
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_parity_large_configs(cfg):
+    V, F = P.mesh_config(cfg)
+    h = P.HostEngine.build(V, F)
+    q = P.gen_queries(cfg, V, F, 0, 200_000)
+    r = P.Engine(h).batch_query(q)
+    ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
+    _compare(r, ref, len(q))
+    _check_counters(r, ref, sequential=False)
