@@ -13,7 +13,7 @@ CXXFLAGS := -O2 -g -std=gnu++17 -fPIC -ffp-contract=off -fvisibility=hidden -pth
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off,-fvisibility=hidden \
             -Xptxas -v --expt-relaxed-constexpr
 
-all: $(LIBDIR)/libp2m_host.so $(LIBDIR)/libp2m_cuda.so oracle
+all: $(LIBDIR)/libp2m_host.so $(LIBDIR)/libp2m_cuda.so oracle examples/query_demo
 
 $(LIBDIR)/libp2m_host.so: $(HOSTSRC) $(HOSTHDR)
 	@mkdir -p $(LIBDIR)
@@ -32,3 +32,6 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+examples/query_demo: examples/query_demo.cpp include/p2m_engine.hpp include/p2m.h $(LIBDIR)/libp2m_host.so $(LIBDIR)/libp2m_cuda.so
+	g++ -O2 -std=c++17 -Iinclude -o $@ $< -L$(LIBDIR) -lp2m_cuda -lp2m_host -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'

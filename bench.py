@@ -150,7 +150,7 @@ def run_reference(args, rank, world):
 
     cfg = args.config
     n_cfg = CONFIG_N[cfg]
-    V, F, h, q, tb = build_workload(cfg, 0, 1, min(n_cfg, args.ref_sample), 0, args.aux_corner_union)
+    V, F, h, q, tb = build_workload(cfg, 0, 1, min(n_cfg, args.ref_sample), 0, (args.aux_table == "corner_union"))
     ref = O.have_reference()
     oe = O.OracleEngine(h.arrays(), reference=ref)
     threads = O.max_threads(ref)
@@ -170,7 +170,7 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic config generator)",
         "impl": "reference",
         "config": {"workload": CONFIG_NAME[cfg], "queries_per_step": n, "build": tb,
-                   "tables": "aux_corner_union" if args.aux_corner_union else "spec_single_ball"},
+                   "tables": args.aux_table},
         "cpu_baseline": {"value": v, "unit": "queries/s", "cores": threads,
                          "kind": "reference" if ref else "port",
                          "sample": f"{n} queries/step of the {CONFIG_NAME[cfg].split(':')[0]} workload"},
@@ -188,7 +188,8 @@ def main():
     ap.add_argument("--queries", type=int, default=0, help="override queries per rank")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
-    ap.add_argument("--aux-corner-union", action="store_true")
+    ap.add_argument("--aux-table", default="corner_union", choices=["corner_union", "ball"],
+                    help="auxiliary-site tables: corner_union (default, REF/SPEC.md:413) or the literal single ball (406-414)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--scan-mode", type=int, default=0, help="0 grouped (default), 1 fused per-row")
@@ -216,7 +217,7 @@ def main():
     cfg = args.config
     n = args.queries or CONFIG_N[cfg]
     ncpu = os.cpu_count() or 1
-    V, F, h, q_host, tb = build_workload(cfg, rank, world, n, max(1, ncpu // world), args.aux_corner_union)
+    V, F, h, q_host, tb = build_workload(cfg, rank, world, n, max(1, ncpu // world), (args.aux_table == "corner_union"))
     st = h.stats()
     eng = P.Engine(h, devices=[dev])
     lib = L.cuda()
@@ -329,7 +330,7 @@ def main():
         "config": {
             "workload": CONFIG_NAME[cfg], "queries_per_rank": n, "parallelism": f"queries sharded x{world}, structure replicated",
             "l2": "inputs larger than L2 (q 24 B + out 44 B per row; structure stays L2-resident by design)",
-            "tables": "aux_corner_union" if args.aux_corner_union else "spec_single_ball (REF/SPEC.md:406-414)",
+            "tables": {"corner_union": "aux corner-union (REF/SPEC.md:413)", "ball": "aux single ball (REF/SPEC.md:406-414)"}[args.aux_table],
             "build": tb, "n_sites": st["n_sites"], "n_faces": st["n_faces"], "list_avg": st["list_avg"],
             "list_max": st["list_max"],
             "per_query": {"candidates": c["candidates_visited"] / n, "exact": c["exact_evaluations"] / n,

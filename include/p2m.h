@@ -154,9 +154,11 @@ typedef struct p2m_build_config {
     double domain_scale;   /* D = AABB scaled about its centre; default 10.0 (REF/SPEC.md:648) */
     int n_threads;         /* 0 = all hardware threads */
     int strict_mesh;       /* --strict-mesh: degenerate faces are an error instead of removed */
-    int aux_corner_union;  /* 0: auxiliary table = one ball B(s, max_u |s-u|+|u-proj|) (REF/SPEC.md:
-                              406-414, default); 1: union of B(u, |u-proj|) over the cell corners --
-                              the tighter superset REF/SPEC.md:413 names as the SPEC list's subset */
+    int aux_corner_union;  /* 1 (default): auxiliary table = union of B(u, |u-proj|) over the cell
+                              corners -- the subset of the SPEC list that REF/SPEC.md:413 names, valid
+                              by Theorem 1 about proj; 0: the literal single ball B(s, max_u |s-u| +
+                              |u-proj|) of REF/SPEC.md:406-414 (whole-mesh lists for off-surface sites
+                              whose cells reach the sentinels) */
 } p2m_build_config;
 
 typedef struct p2m_build_stats {

@@ -61,7 +61,7 @@ P2M_API void p2m_build_config_default(p2m_build_config* c) {
     c->domain_scale = 10.0;
     c->n_threads = 0;
     c->strict_mesh = 0;
-    c->aux_corner_union = 0;
+    c->aux_corner_union = 1;
 }
 
 P2M_API int p2m_build(const double* vertices, uint64_t n_vertices, const uint32_t* faces,

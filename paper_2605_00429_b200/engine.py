@@ -46,7 +46,7 @@ class BuildConfig:
     domain_scale: float = 10.0
     n_threads: int = 0
     strict_mesh: bool = False
-    aux_corner_union: bool = False
+    aux_corner_union: bool = True
 
     def to_c(self) -> L.BuildConfig:
         c = L.BuildConfig()

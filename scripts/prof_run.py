@@ -10,12 +10,12 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--mode", type=int, default=0)
-ap.add_argument("--aux-corner-union", action="store_true")
+ap.add_argument("--aux-ball", action="store_true")
 a = ap.parse_args()
 N = {1: 1_000_000, 2: 10_000_000, 3: 20_000_000, 4: 100_000_000, 5: 100_000_000}
 n = a.n or N[a.config]
 V, F = P.mesh_config(a.config)
-h = P.HostEngine.build(V, F, P.BuildConfig(aux_corner_union=a.aux_corner_union))
+h = P.HostEngine.build(V, F, P.BuildConfig(aux_corner_union=not a.aux_ball))
 q = P.gen_queries(a.config, V, F, 0, n)
 eng = P.Engine(h)
 lib = L.cuda()

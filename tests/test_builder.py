@@ -141,8 +141,9 @@ def test_augmentation_behaviour():
 
 def test_aux_corner_union_is_subset_and_valid():
     V, F = bumpy_sphere(3, seed=2)
-    h1 = P.HostEngine.build(V, F)
+    h1 = P.HostEngine.build(V, F, P.BuildConfig(aux_corner_union=False))
     h2 = P.HostEngine.build(V, F, P.BuildConfig(aux_corner_union=True))
+    assert superset_check(h1, nq=800) == 0
     a1, a2 = h1.arrays(), h2.arrays()
     assert np.array_equal(a1["site_xyz"], a2["site_xyz"])
     for s in np.flatnonzero(a1["site_kind"] == L.SITE_AUXILIARY):
