@@ -58,33 +58,56 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled every 10 ms DURING the timed region (NVML in-process;
+    nvidia-smi polling as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_s: float = 0.01):
         self.gpu = gpu
-        self.samples = []
+        self.period = period_s
+        self.samples = []  # (sm_mhz, max_mhz, reason_bits)
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvml"
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml as N
+
+        N.nvmlInit()
+        try:
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            h = N.nvmlDeviceGetHandleByIndex(idx)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or N.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self._stop.is_set():
+                self.samples.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM), mx, int(get_r(h))))
+                self._stop.wait(self.period)
+        finally:
+            N.nvmlShutdown()
+
+    def _run_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active")
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={fields}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                                     timeout=5).stdout.strip().split(",")
+                self.samples.append((float(out[0]), float(out[1]), int(out[2].strip(), 16)))
             except Exception:
                 pass
             self._stop.wait(0.2)
 
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self.source = "nvidia-smi"
+            self._run_smi()
+
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
@@ -95,13 +118,13 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+        bits = 0
+        for _, _, b in self.samples:
+            bits |= b
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(v for k, v in names.items() if bits & k), "samples": len(self.samples),
+                "source": self.source}
 
 
 def build_workload(cfg, rank, world, n_per_rank, build_threads, aux_corner_union):
@@ -182,7 +205,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--queries", type=int, default=0, help="override queries per rank")
@@ -338,7 +361,7 @@ def main():
             "split_ms": {"morton": split[0], "sort": split[1], "descend": split[2], "regroup_sort": split[3], "scan": split[4], "total": split[5]},
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_scan_grouped (site-tiled pruned list scan, exact fp64)",
+                     "traffic": traffic, "kernel": "k_scan_tiles (site-tiled pruned list scan, exact fp64)",
                      "algorithmic_bytes_per_launch": B_scan,
                      "bytes_per_query": "72 + 36 C_q + 72 E_q (SURVEY.md 8(d) minus the 32 n_q of the descent kernel)",
                      "pipeline_algorithmic_gbs": pipeline_gbs, "pipeline_bytes_per_step": B_alg,

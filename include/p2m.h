@@ -70,6 +70,9 @@ typedef struct p2m_engine_desc {
     const uint32_t *list_faces;  /* list_offsets[n_sites] face ids, ascending & unique per site */
     double domain_min[3];        /* query domain D (REF/SPEC.md:648: 10x mesh AABB) */
     double domain_max[3];
+    const double *site_cell_box; /* optional (may be NULL): 6 * n_sites, AABB (min.xyz, max.xyz) of each
+                                    site's Voronoi cell (NaN for sentinels).  Enables the exact grid
+                                    cell-locate of nearest_site; without it the k-d tree is used. */
 } p2m_engine_desc;
 
 /* Aggregate counters (REF/SPEC.md:468, 500, 511). */

@@ -42,6 +42,7 @@ class EngineDesc(C.Structure):
         ("list_faces", u32p),
         ("domain_min", C.c_double * 3),
         ("domain_max", C.c_double * 3),
+        ("site_cell_box", dp),
     ]
 
 

@@ -99,7 +99,28 @@ struct Params {
     float f32_delta;        // additive slack of the conservative fp32 sphere pre-filter
     const uint8_t* heavy;   // per site: 1 if its rows are tiled long_tile rows per CTA
     uint32_t long_tile;     // (32, 64, 128 or 256)
+    // exact grid cell-locate (optional, grid_off == nullptr -> k-d tree only): every site whose
+    // Voronoi cell box meets grid cell c is listed in grid_site[grid_off[c] .. grid_off[c+1])
+    const D4* site_pos;     // by site id: {x, y, z, meta (sentinel bit)}
+    const uint32_t* grid_off;
+    const uint32_t* grid_site;
+    double grid_lo[3], grid_inv[3];
+    uint32_t grid_res[3];
 };
+
+// Grid cell of q; false if q lies outside the grid box (the caller then uses the k-d tree).  The
+// host rasterises cell boxes with exactly this formula, and (x - lo) * inv is monotone in x, so q
+// inside a box always maps to a cell inside the box's cell range.
+__device__ __forceinline__ bool grid_cell(const Params& p, V q, uint32_t* cell) {
+    const double fx = (q.x - p.grid_lo[0]) * p.grid_inv[0];
+    const double fy = (q.y - p.grid_lo[1]) * p.grid_inv[1];
+    const double fz = (q.z - p.grid_lo[2]) * p.grid_inv[2];
+    if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < (double)p.grid_res[0] && fy < (double)p.grid_res[1] &&
+          fz < (double)p.grid_res[2]))
+        return false;
+    *cell = ((uint32_t)fz * p.grid_res[1] + (uint32_t)fy) * p.grid_res[0] + (uint32_t)fx;
+    return true;
+}
 
 }  // namespace dev
 }  // namespace p2m

@@ -156,12 +156,20 @@ struct Slot {
     uint64_t* off = nullptr;
     uint32_t *lf = nullptr, *bvh_perm = nullptr;
     uint8_t* heavy = nullptr;
+    D4* site_pos = nullptr;
+    uint32_t *grid_off = nullptr, *grid_site = nullptr;
     Params params{};
     std::mutex mu;
-    // host-API workspace
-    double *q = nullptr, *dist = nullptr, *cp = nullptr;
-    uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
+    // host-API path: kPipe streams, each with a chunk-sized staging set, so the H2D copy of one
+    // chunk, the kernels of another and the D2H copy of a third overlap
+    static constexpr int kPipe = 3;
+    cudaStream_t pipe[kPipe] = {nullptr, nullptr, nullptr};
+    struct Ws {
+        double *q = nullptr, *dist = nullptr, *cp = nullptr;
+        uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
+    } ws[kPipe];
     uint64_t cap = 0;
+    cudaEvent_t agg_ready = nullptr;
     unsigned long long* agg = nullptr;
     // profiling: ring of event sets, read lazily by p2m_last_timings (no host sync per call)
     static constexpr int kRing = 256;
@@ -178,7 +186,9 @@ struct p2m_engine {
     uint64_t bytes = 0;
     bool profiling = false;
     int scan_mode = P2M_SCAN_GROUPED;
+    int e2e_chunks = 4;  // host-buffer path pipeline depth (P2M_E2E_CHUNKS overrides)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
+    uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
 };
 
 namespace {
@@ -187,17 +197,118 @@ void free_slot(Slot& s) {
     cudaSetDevice(s.dev);
     cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
     cudaFree(s.heavy);
+    cudaFree(s.site_pos); cudaFree(s.grid_off); cudaFree(s.grid_site);
     cudaFree(s.f32);
-    cudaFree(s.q); cudaFree(s.dist); cudaFree(s.cp); cudaFree(s.face); cudaFree(s.site); cudaFree(s.flags);
+    for (auto& w : s.ws) {
+        cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
+    }
+    for (auto& st : s.pipe) if (st) cudaStreamDestroy(st);
+    if (s.agg_ready) cudaEventDestroy(s.agg_ready);
     cudaFree(s.agg);
     for (auto& e : s.ev) if (e) cudaEventDestroy(e);
     s.ev.clear();
     if (s.stream) cudaStreamDestroy(s.stream);
 }
 
+// Exact cell-locate grid over the Morton key box (1.5x the real sites' AABB): cubic cells, about 16
+// per real site, at most 512 per axis; site s is listed in every cell its Voronoi cell box (inflated
+// by 1e-9 |D|) meets.  Built only when (1) every real site has a box and (2) no sentinel can be
+// nearest anywhere in the grid box: with s0 the real site nearest the box centre, every point x of
+// the box has d(x, nearest real) <= max_corner |corner - s0| < min_k d(sentinel_k, box).
+struct Grid {
+    double lo[3] = {0, 0, 0}, inv[3] = {0, 0, 0};
+    uint32_t res[3] = {0, 0, 0};
+    std::vector<uint32_t> off, site;
+};
+
+bool build_grid(const p2m_engine_desc* d, const double* key_lo, const double* key_ext, Grid& g) {
+    if (!d->site_cell_box) return false;
+    const uint64_t S = d->n_sites;
+    double hi[3], c[3];
+    for (int k = 0; k < 3; ++k) { hi[k] = key_lo[k] + key_ext[k]; c[k] = 0.5 * (key_lo[k] + hi[k]); }
+    uint64_t n_real = 0, s0 = UINT64_MAX;
+    double best = INFINITY;
+    for (uint64_t s = 0; s < S; ++s) {
+        if (d->site_kind[s] == P2M_SITE_SENTINEL) continue;
+        ++n_real;
+        const double* b = d->site_cell_box + 6 * s;
+        for (int k = 0; k < 6; ++k) if (!std::isfinite(b[k])) return false;
+        const double* p = d->site_xyz + 3 * s;
+        const double dd = (p[0] - c[0]) * (p[0] - c[0]) + (p[1] - c[1]) * (p[1] - c[1]) + (p[2] - c[2]) * (p[2] - c[2]);
+        if (dd < best) { best = dd; s0 = s; }
+    }
+    if (!n_real) return false;
+    double rmax = 0.0;
+    for (int i = 0; i < 8; ++i) {
+        double dd = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double x = (i >> k & 1) ? hi[k] : key_lo[k];
+            dd += (x - d->site_xyz[3 * s0 + k]) * (x - d->site_xyz[3 * s0 + k]);
+        }
+        rmax = std::max(rmax, std::sqrt(dd));
+    }
+    for (uint64_t s = 0; s < S; ++s) {
+        if (d->site_kind[s] != P2M_SITE_SENTINEL) continue;
+        double dd = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double x = d->site_xyz[3 * s + k];
+            const double t = x < key_lo[k] ? key_lo[k] - x : (x > hi[k] ? x - hi[k] : 0.0);
+            dd += t * t;
+        }
+        if (!(std::sqrt(dd) > rmax * (1.0 + 1e-9))) return false;
+    }
+    const double vol = key_ext[0] * key_ext[1] * key_ext[2];
+    const double cell = std::cbrt(vol / (16.0 * (double)n_real));
+    for (int k = 0; k < 3; ++k) {
+        g.lo[k] = key_lo[k];
+        g.res[k] = (uint32_t)std::min(512.0, std::max(1.0, std::ceil(key_ext[k] / cell)));
+        g.inv[k] = (double)g.res[k] / key_ext[k];
+    }
+    double dspan = 0.0;
+    for (int k = 0; k < 3; ++k) dspan += (d->domain_max[k] - d->domain_min[k]) * (d->domain_max[k] - d->domain_min[k]);
+    const double margin = 1e-9 * std::sqrt(dspan);
+    const uint64_t ncell = (uint64_t)g.res[0] * g.res[1] * g.res[2];
+    auto range = [&](const double* b, uint32_t* i0, uint32_t* i1) {
+        for (int k = 0; k < 3; ++k) {
+            const double a = (b[k] - margin - g.lo[k]) * g.inv[k], z = (b[3 + k] + margin - g.lo[k]) * g.inv[k];
+            if (z < 0.0 || a >= (double)g.res[k]) return false;
+            i0[k] = a <= 0.0 ? 0u : (uint32_t)std::min<double>(std::floor(a), g.res[k] - 1);
+            i1[k] = z <= 0.0 ? 0u : (uint32_t)std::min<double>(std::floor(z), g.res[k] - 1);
+        }
+        return true;
+    };
+    std::vector<uint64_t> cnt(ncell + 1, 0);
+    uint32_t i0[3], i1[3];
+    for (int pass = 0; pass < 2; ++pass) {
+        std::vector<uint64_t> cur;
+        if (pass == 1) {
+            for (uint64_t cidx = 0; cidx < ncell; ++cidx) cnt[cidx + 1] += cnt[cidx];
+            if (cnt[ncell] >= (1ull << 32)) return false;
+            g.site.resize(cnt[ncell]);
+            cur.assign(cnt.begin(), cnt.end() - 1);
+        }
+        for (uint64_t s = 0; s < S; ++s) {
+            if (d->site_kind[s] == P2M_SITE_SENTINEL) continue;
+            if (!range(d->site_cell_box + 6 * s, i0, i1)) continue;
+            for (uint32_t z = i0[2]; z <= i1[2]; ++z)
+                for (uint32_t y = i0[1]; y <= i1[1]; ++y)
+                    for (uint32_t x = i0[0]; x <= i1[0]; ++x) {
+                        const uint64_t cidx = ((uint64_t)z * g.res[1] + y) * g.res[0] + x;
+                        if (pass == 0) ++cnt[cidx + 1];
+                        else g.site[cur[cidx]++] = (uint32_t)s;
+                    }
+        }
+    }
+    g.off.resize(ncell + 1);
+    for (uint64_t cidx = 0; cidx <= ncell; ++cidx) g.off[cidx] = (uint32_t)cnt[cidx];
+    return true;
+}
+
 int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    for (auto& st : s.pipe) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s.agg_ready, cudaEventDisableTiming));
     CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
@@ -207,6 +318,11 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.bvh_perm, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.agg, sizeof(unsigned long long) * 8));
     CK(cudaMalloc(&s.heavy, std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMalloc(&s.site_pos, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    if (E.grid_cells) {
+        CK(cudaMalloc(&s.grid_off, 4 * (E.grid_cells + 1)));
+        CK(cudaMalloc(&s.grid_site, 4 * std::max<uint64_t>(1, E.grid_pairs)));
+    }
     CK(cudaMemset(s.heavy, 0, std::max<uint64_t>(1, E.n_sites)));
     s.ev.assign(Slot::kEv * Slot::kRing, nullptr);
     for (auto& e : s.ev) CK(cudaEventCreate(&e));
@@ -221,21 +337,25 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
 
 int ensure_ws(Slot& s, uint64_t n) {
     if (n <= s.cap) return P2M_OK;
-    cudaFree(s.q); cudaFree(s.dist); cudaFree(s.cp); cudaFree(s.face); cudaFree(s.site); cudaFree(s.flags);
+    CK(cudaDeviceSynchronize());
     s.cap = 0;
-    CK(cudaMalloc(&s.q, 24 * n));
-    CK(cudaMalloc(&s.dist, 8 * n));
-    CK(cudaMalloc(&s.cp, 24 * n));
-    CK(cudaMalloc(&s.face, 4 * n));
-    CK(cudaMalloc(&s.site, 4 * n));
-    CK(cudaMalloc(&s.flags, 4 * n));
+    for (auto& w : s.ws) {
+        cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
+        w = Slot::Ws{};
+        CK(cudaMalloc(&w.q, 24 * n));
+        CK(cudaMalloc(&w.dist, 8 * n));
+        CK(cudaMalloc(&w.cp, 24 * n));
+        CK(cudaMalloc(&w.face, 4 * n));
+        CK(cudaMalloc(&w.site, 4 * n));
+        CK(cudaMalloc(&w.flags, 4 * n));
+    }
     s.cap = n;
     return P2M_OK;
 }
 
 // Morton keys -> sort -> fused query.  rows_out (optional) receives the sorted row order.
 int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2m::dev::Out& o, bool counters,
-                 cudaStream_t st, bool nearest_only, uint32_t* d_site_only) {
+                 cudaStream_t st, bool nearest_only, uint32_t* d_site_only, bool allow_prof = true) {
     if (n >= (1ull << 32)) { set_err("p2m_query_device: at most 2^32-1 rows per call"); return P2M_ERR_INVALID; }
     CK(cudaSetDevice(s.dev));
     uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
@@ -256,7 +376,7 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         CK(cudaMallocAsync(&tiles, 4 * p2m::dev::max_tiles(n, E->n_sites), st));
         CK(cudaMallocAsync(&meta, 16, st));
     }
-    const bool prof = E->profiling && s.recorded < Slot::kRing;
+    const bool prof = allow_prof && E->profiling && s.recorded < Slot::kRing;
     cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * s.recorded] : nullptr;
     if (prof) { CK(cudaEventRecord(ev[0], st)); ++s.recorded; }
     CK(p2m::dev::launch_morton(d_q, n, s.params, keys, rows, st));
@@ -443,6 +563,21 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         P.key_scale[c] = 1024.0 / (2.0 * h);
     }
 
+    Grid grid;
+    {
+        double ext[3];
+        for (int c = 0; c < 3; ++c) ext[c] = 1024.0 / P.key_scale[c];
+        if (build_grid(d, P.key_lo, ext, grid)) {
+            E->grid_cells = (uint64_t)grid.res[0] * grid.res[1] * grid.res[2];
+            E->grid_pairs = grid.site.size();
+            for (int c = 0; c < 3; ++c) { P.grid_lo[c] = grid.lo[c]; P.grid_inv[c] = grid.inv[c]; P.grid_res[c] = grid.res[c]; }
+        }
+        if (std::getenv("P2M_NO_GRID")) E->grid_cells = E->grid_pairs = 0;
+    }
+    std::vector<D4> site_pos(S);
+    for (uint64_t i = 0; i < S; ++i)
+        site_pos[i] = D4{d->site_xyz[3 * i], d->site_xyz[3 * i + 1], d->site_xyz[3 * i + 2],
+                         bits_to_double(d->site_kind[i] == P2M_SITE_SENTINEL ? (1ull << 34) : 0ull)};
     // ---- upload to the first device, peer-replicate to the rest ----
     for (int k = 0; k < n_devices; ++k) {
         auto s = std::make_unique<Slot>();
@@ -464,12 +599,16 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
             cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.site_pos, site_pos.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            (E->grid_cells && cudaMemcpy(s0.grid_off, grid.off.data(), 4 * (E->grid_cells + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
+            (E->grid_pairs && cudaMemcpy(s0.grid_site, grid.site.data(), 4 * E->grid_pairs, cudaMemcpyHostToDevice) != cudaSuccess)) {
             set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
             return fail(P2M_ERR_CUDA);
         }
     }
-    E->bytes = sizeof(D4) * (S + 4 * F + bvh.nodes.size()) + sizeof(float4) * F + 8 * (S + 1) + 4 * (L + F) + S;
+    E->bytes = sizeof(D4) * (2 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * F + 8 * (S + 1) + 4 * (L + F) + S +
+               (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0);
     auto t0 = std::chrono::steady_clock::now();
     for (size_t k = 1; k < E->slots.size(); ++k) {
         Slot& s = *E->slots[k];
@@ -486,7 +625,10 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         struct { void* dst; const void* src; size_t n; } cp[] = {
             {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
             {s.off, s0.off, 8 * (S + 1)},
-            {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F}};
+            {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
+            {s.site_pos, s0.site_pos, sizeof(D4) * S},
+            {s.grid_off, s0.grid_off, E->grid_cells ? 4 * (E->grid_cells + 1) : 0},
+            {s.grid_site, s0.grid_site, 4 * E->grid_pairs}};
         for (auto& c : cp)
             if (c.n && cudaMemcpyPeerAsync(c.dst, s.dev, c.src, s0.dev, c.n, s.stream) != cudaSuccess) {
                 set_err("p2m_engine_create: peer copy failed");
@@ -502,7 +644,11 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         s->params = P;
         s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.off = s->off; s->params.lf = s->lf;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
+        s->params.site_pos = s->site_pos;
+        s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
+        s->params.grid_site = s->grid_site;
     }
+    if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(1, std::atoi(v));
     {
         int rc = mark_heavy_sites(E.get(), d);
         if (rc != P2M_OK) return fail(rc);
@@ -603,21 +749,34 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
         std::lock_guard<std::mutex> lk(s.mu);
         auto run = [&]() -> int {
             CK(cudaSetDevice(s.dev));
-            int rc = ensure_ws(s, m);
+            // chunking: at least 1 Mi rows per chunk, about e->e2e_chunks chunks for large shards
+            const uint64_t nch = (uint64_t)std::max(1, e->e2e_chunks);
+            const uint64_t chunk = std::min<uint64_t>(m, std::max<uint64_t>(1ull << 20, (m + nch - 1) / nch));
+            int rc = ensure_ws(s, chunk);
             if (rc != P2M_OK) return rc;
-            CK(cudaMemcpyAsync(s.q, q + 3 * b, 24 * m, cudaMemcpyHostToDevice, s.stream));
-            p2m::dev::Out o{s.dist, s.cp, s.face, s.site, s.flags, nullptr, cnt ? s.agg : nullptr};
-            if (cnt) CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.stream));
-            rc = run_pipeline(e, s, s.q, m, o, cnt != nullptr, s.stream, false, nullptr);
-            if (rc != P2M_OK) return rc;
-            CK(cudaMemcpyAsync(dist + b, s.dist, 8 * m, cudaMemcpyDeviceToHost, s.stream));
-            CK(cudaMemcpyAsync(cp + 3 * b, s.cp, 24 * m, cudaMemcpyDeviceToHost, s.stream));
-            CK(cudaMemcpyAsync(face + b, s.face, 4 * m, cudaMemcpyDeviceToHost, s.stream));
-            CK(cudaMemcpyAsync(site + b, s.site, 4 * m, cudaMemcpyDeviceToHost, s.stream));
-            if (flags) CK(cudaMemcpyAsync(flags + b, s.flags, 4 * m, cudaMemcpyDeviceToHost, s.stream));
+            if (cnt) {
+                CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.pipe[0]));
+                CK(cudaEventRecord(s.agg_ready, s.pipe[0]));
+                for (int k = 1; k < Slot::kPipe; ++k) CK(cudaStreamWaitEvent(s.pipe[k], s.agg_ready, 0));
+            }
+            int c = 0;
+            for (uint64_t off = 0; off < m; off += chunk, ++c) {
+                const uint64_t len = std::min(chunk, m - off), r0 = b + off;
+                cudaStream_t st = s.pipe[c % Slot::kPipe];
+                Slot::Ws& w = s.ws[c % Slot::kPipe];  // reused only after this stream's previous D2H
+                CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, st));
+                p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
+                rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false);
+                if (rc != P2M_OK) return rc;
+                CK(cudaMemcpyAsync(dist + r0, w.dist, 8 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(cp + 3 * r0, w.cp, 24 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(face + r0, w.face, 4 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(site + r0, w.site, 4 * len, cudaMemcpyDeviceToHost, st));
+                if (flags) CK(cudaMemcpyAsync(flags + r0, w.flags, 4 * len, cudaMemcpyDeviceToHost, st));
+            }
+            for (auto& st : s.pipe) CK(cudaStreamSynchronize(st));
             unsigned long long h[8] = {0};
-            if (cnt) CK(cudaMemcpyAsync(h, s.agg, sizeof h, cudaMemcpyDeviceToHost, s.stream));
-            CK(cudaStreamSynchronize(s.stream));
+            if (cnt) CK(cudaMemcpy(h, s.agg, sizeof h, cudaMemcpyDeviceToHost));
             parts[g].n_queries = m;
             parts[g].candidates_visited = h[0];
             parts[g].exact_evaluations = h[1];

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_descend(Params p, const double* __restr
     if (i < n) {
         const uint32_t row = rows[i];
         const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
-        const NN nn = nearest_site(p, q);
+        const NN nn = nearest_site_cl(p, q);
         visited = nn.visited;
         const bool in_d = q.x >= p.dmin[0] && q.x <= p.dmax[0] && q.y >= p.dmin[1] && q.y <= p.dmax[1] &&
                           q.z >= p.dmin[2] && q.z <= p.dmax[2];
@@ -273,23 +273,35 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                 const int kk = __ffs(um) - 1;
                 um &= um - 1;
                 if ((mask >> kk) & 1u) {
+                    // The conservative fp32 test above already pruned everything the oracle's fp64
+                    // sphere test would prune except a sliver within its margin; re-testing in fp64
+                    // would cost a dependent 32-byte load and ~15 DP ops per survivor, while
+                    // evaluating a few extra candidates exactly can never change the minimum.  (The
+                    // fused path keeps the fp64 test, so its counters match the oracle exactly.)
+                    // the batch mask used the d_min of the batch start: re-test this candidate with
+                    // the current one (same conservative fp32 test, operands already in smem)
+                    {
+                        const int k = k0 + kk, pp = k >> 1, h = k & 1;
+                        float dkx, dky;
+                        upk2(DK, dkx, dky);
+                        const float dx = __uint_as_float((uint32_t)QX) - s_pf[8 * pp + h];
+                        const float dy = __uint_as_float((uint32_t)QY) - s_pf[8 * pp + 2 + h];
+                        const float dz = __uint_as_float((uint32_t)QZ) - s_pf[8 * pp + 4 + h];
+                        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                        const float th = __fadd_ru(s_pf[8 * pp + 6 + h], dkx);
+                        if (d2f > __fmul_ru(th, th)) continue;
+                    }
                     const uint32_t f = s_fid[k0 + kk];
-                    const D4* rec = p.rec + 4 * (uint64_t)f;   // same address across the warp
-                    const D4 sp = ldg4(rec);
-                    const double dc2 = vd2(q, V{sp.x, sp.y, sp.z});
-                    const double t = sp.w + dmin + p.prune_eps;
-                    if (!(dc2 > t * t)) {
-                        V a, bb3, c3, pp3;
-                        load_tri(rec, &a, &bb3, &c3);
-                        const double dd = closest_tri(q, a, bb3, c3, &pp3);
-                        ++exact;
-                        if (dd < best || (dd == best && f < bf)) {
-                            best = dd;
-                            bf = f;
-                            dmin = sqrt(dd);
-                            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
-                            DK = pk2(dkf, dkf);
-                        }
+                    V a, bb3, c3, pp3;
+                    load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
+                    const double dd = closest_tri(q, a, bb3, c3, &pp3);
+                    ++exact;
+                    if (dd < best || (dd == best && f < bf)) {
+                        best = dd;
+                        bf = f;
+                        dmin = sqrt(dd);
+                        const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+                        DK = pk2(dkf, dkf);
                     }
                 }
             }

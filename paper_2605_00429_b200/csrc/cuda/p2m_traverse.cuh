@@ -50,6 +50,30 @@ __device__ __forceinline__ NN nearest_site(const Params& p, V q) {
     return r;
 }
 
+// nearest_site through the grid when q is inside the grid box: the exact lexicographic (d^2, id)
+// minimum over every site whose Voronoi cell box meets q's grid cell -- a superset of the sites
+// whose (closed) cell contains q, so it is the exact nearest site with lowest-id ties.  Falls back
+// to the k-d tree outside the grid box or when the engine has no grid.
+__device__ __forceinline__ NN nearest_site_cl(const Params& p, V q) {
+    uint32_t c;
+    if (!p.grid_off || !grid_cell(p, q, &c)) return nearest_site(p, q);
+    NN r{__longlong_as_double(0x7ff0000000000000ll), 0xffffffffu, 0u, false};
+    const uint32_t b = p.grid_off[c], e = p.grid_off[c + 1];
+    if (b == e) return nearest_site(p, q);
+    for (uint32_t j = b; j < e; ++j) {
+        const uint32_t id = p.grid_site[j];
+        const D4 s = ldg4(p.site_pos + id);
+        const double dd = vd2(q, V{s.x, s.y, s.z});
+        ++r.visited;
+        if (dd < r.d2 || (dd == r.d2 && id < r.id)) {
+            r.d2 = dd;
+            r.id = id;
+            r.sentinel = ((uint64_t)__double_as_longlong(s.w) & kSentinelBit) != 0;
+        }
+    }
+    return r;
+}
+
 // Exact global closest point by the fallback BVH (REF/SPEC.md:201-209, 491): lowest face id on
 // exact d^2 ties; a node is skipped only when its box is farther than best*(1+1e-12).
 __device__ __forceinline__ uint32_t bvh_closest(const Params& p, V q, double* best_out) {

@@ -315,6 +315,7 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
     Timer tt;
     const uint64_t S = h.sites.size();
     std::vector<std::vector<uint32_t>> per(S);
+    h.cell_box.assign(6 * S, std::nan(""));
     std::vector<uint64_t> ncorner(threads, 0);
     double t_cells = 0.0;
     std::vector<double> tcell(threads, 0.0);
@@ -330,6 +331,12 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
             cc.compute((uint32_t)s, corners, nullptr);
             tcell[w] += tc.s();
             ncorner[w] += corners.size();
+            {
+                Box cb;
+                for (const V3& u : corners) cb.add(u);
+                double* o = &h.cell_box[6 * s];
+                o[0] = cb.lo.x; o[1] = cb.lo.y; o[2] = cb.lo.z; o[3] = cb.hi.x; o[4] = cb.hi.y; o[5] = cb.hi.z;
+            }
             const V3 site = h.sites[s];
             balls.clear();
             // closed balls (REF/SPEC.md:95), inflated by a relative 1e-10 and 1e-12*diag(D) so

@@ -35,6 +35,7 @@ struct HostEngine {
     std::vector<double> site_xyz;
     std::vector<uint8_t> kind;
     std::vector<double> refs;    // aux projection (3 per site, NaN otherwise)
+    std::vector<double> cell_box;  // AABB of each site's Voronoi cell corners (6 per site, NaN for sentinels)
     uint32_t sentinel_ids[8];
     // interception index (REF/SPEC.md:391-394) as CSR
     std::vector<uint64_t> off;

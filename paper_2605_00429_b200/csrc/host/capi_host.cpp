@@ -90,6 +90,7 @@ P2M_API int p2m_host_engine_desc(const p2m_host_engine* he, p2m_engine_desc* d) 
         d->face_sphere = h.sphere.data();
         d->list_offsets = h.off.data();
         d->list_faces = h.lists.data();
+        d->site_cell_box = h.cell_box.empty() ? nullptr : h.cell_box.data();
         d->domain_min[0] = h.D.lo.x; d->domain_min[1] = h.D.lo.y; d->domain_min[2] = h.D.lo.z;
         d->domain_max[0] = h.D.hi.x; d->domain_max[1] = h.D.hi.y; d->domain_max[2] = h.D.hi.z;
         return (int)P2M_OK;
@@ -151,7 +152,7 @@ P2M_API int p2m_host_closest_point(const p2m_host_engine* he, const double* q, d
 // EngineIndexFile (REF/SPEC.md:588-591): magic "P2MX", LE u32 version, mesh hash, D, sites
 // (kind, position, reference), per-site table offsets + face ids, config echo.  The BVH and the
 // NNS index are rebuilt on load (REF/SPEC.md:639).
-static const uint32_t kFileVersion = 1;
+static const uint32_t kFileVersion = 2;  // v2 adds the Voronoi cell boxes
 
 P2M_API int p2m_host_engine_save(const p2m_host_engine* he, const char* path) {
     return guarded([&] {
@@ -176,6 +177,7 @@ P2M_API int p2m_host_engine_save(const p2m_host_engine* he, const char* path) {
         w(h.sentinel_ids, sizeof h.sentinel_ids);
         w(h.off.data(), 8 * (S + 1));
         w(h.lists.data(), 4 * h.lists.size());
+        w(h.cell_box.data(), 8 * h.cell_box.size());
         w("XM2P", 4);
         ok = (std::fclose(fp) == 0) && ok;
         if (!ok) { set_error("write failed"); return (int)P2M_ERR_IO; }
@@ -235,6 +237,8 @@ P2M_API int p2m_host_engine_load(const char* path, const double* vertices, uint6
         if (!ok || h.off[S] > (1ull << 36)) { std::fclose(fp); set_error("EngineIndexFile truncated (tables)"); return (int)P2M_ERR_IO; }
         h.lists.resize(h.off[S]);
         r(h.lists.data(), 4 * h.lists.size());
+        h.cell_box.resize(6 * S);
+        r(h.cell_box.data(), 8 * h.cell_box.size());
         char tail[4] = {0};
         r(tail, 4);
         std::fclose(fp);
