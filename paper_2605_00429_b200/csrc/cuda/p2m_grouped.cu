@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                                                          const uint32_t* __restrict__ meta, Out o) {
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
+    __shared__ D4 s_tri[kChunk * 3];             // the chunk's triangles (96 B each) for the rare path
     __shared__ double s_rd[kTile];
     __shared__ uint32_t s_rf[kTile];
     __shared__ uint32_t s_re[kTile];
@@ -235,6 +236,12 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
             const int pp = tid >> 1, h = tid & 1;
             if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
             s_fid[tid] = nf;
+            if (tid < mc) {  // stage the triangle: the rare path then reads broadcast shared memory
+                const D4* rec = p.rec + 4 * (uint64_t)nf;
+                s_tri[3 * tid] = ldg4(rec + 1);
+                s_tri[3 * tid + 1] = ldg4(rec + 2);
+                s_tri[3 * tid + 2] = ldg4(rec + 3);
+            }
             s_pf[8 * pp + h] = nv.x;
             s_pf[8 * pp + 2 + h] = nv.y;
             s_pf[8 * pp + 4 + h] = nv.z;
@@ -292,9 +299,9 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                         if (d2f > __fmul_ru(th, th)) continue;
                     }
                     const uint32_t f = s_fid[k0 + kk];
-                    V a, bb3, c3, pp3;
-                    load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
-                    const double dd = closest_tri(q, a, bb3, c3, &pp3);
+                    const D4 t0 = s_tri[3 * (k0 + kk)], t1 = s_tri[3 * (k0 + kk) + 1], t2 = s_tri[3 * (k0 + kk) + 2];
+                    V pp3;
+                    const double dd = closest_tri(q, V{t0.x, t0.y, t0.z}, V{t0.w, t1.x, t1.y}, V{t1.z, t1.w, t2.x}, &pp3);
                     ++exact;
                     if (dd < best || (dd == best && f < bf)) {
                         best = dd;
