@@ -145,13 +145,22 @@ def build_workload(cfg, rank, world, n_per_rank, build_threads, aux_corner_union
     return V, F, h, q, {"mesh_s": round(t_mesh, 3), "build_s": round(t_build, 3), "queries_s": round(t_q, 3)}
 
 
+def host_cores():
+    """All host cores this process may use (torchrun exports OMP_NUM_THREADS=1; the CPU baseline
+    deliberately ignores that and runs one OpenMP thread per core)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_oracle_rate(h, q, target_s=12.0, reference=True, threads=0):
     """Queries/s of the CPU query path on a bounded sample (prefix of the same workload)."""
     import oracle as O
 
     ref = reference and O.have_reference()
     oe = O.OracleEngine(h.arrays(), reference=ref)
-    threads = threads or O.max_threads(ref)
+    threads = threads or host_cores()
     n0 = min(len(q), 20000)
     t0 = time.perf_counter()
     oe.batch_query(q[:n0], prune=O.PRUNE_SAFE, threads=threads)
@@ -176,7 +185,7 @@ def run_reference(args, rank, world):
     V, F, h, q, tb = build_workload(cfg, 0, 1, min(n_cfg, args.ref_sample), 0, (args.aux_table == "corner_union"))
     ref = O.have_reference()
     oe = O.OracleEngine(h.arrays(), reference=ref)
-    threads = O.max_threads(ref)
+    threads = host_cores()
     n = len(q)
     for _ in range(args.warmup):
         oe.batch_query(q[: min(n, 20000)], threads=threads)
@@ -232,8 +241,15 @@ def main():
     from paper_2605_00429_b200 import shard
 
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU over NCCL; the data path has no collective (barriers and the max-over-ranks
+        # step time only).  If ranks must share a GPU (a smoke test on a 1-GPU box), NCCL refuses
+        # duplicate devices, so the control plane falls back to gloo.
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(local % ndev)
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()

@@ -73,6 +73,10 @@ typedef struct p2m_engine_desc {
     const double *site_cell_box; /* optional (may be NULL): 6 * n_sites, AABB (min.xyz, max.xyz) of each
                                     site's Voronoi cell (NaN for sentinels).  Enables the exact grid
                                     cell-locate of nearest_site; without it the k-d tree is used. */
+    const double *site_ref_xyz;  /* optional (may be NULL): 3 * n_sites, a point ON the mesh per site --
+                                    auxiliary sites' projection proj(s, M) (REF/SPEC.md:238); ignored
+                                    for mesh vertices (the vertex itself) and sentinels.  Seeds the
+                                    grouped scan's d_min with the upper bound |q - ref| (result-neutral). */
 } p2m_engine_desc;
 
 /* Aggregate counters (REF/SPEC.md:468, 500, 511). */

@@ -43,6 +43,7 @@ class EngineDesc(C.Structure):
         ("domain_min", C.c_double * 3),
         ("domain_max", C.c_double * 3),
         ("site_cell_box", dp),
+        ("site_ref_xyz", dp),
     ]
 
 

@@ -102,6 +102,8 @@ struct Params {
     // exact grid cell-locate (optional, grid_off == nullptr -> k-d tree only): every site whose
     // Voronoi cell box meets grid cell c is listed in grid_site[grid_off[c] .. grid_off[c+1])
     const D4* site_pos;     // by site id: {x, y, z, meta (sentinel bit)}
+    const D4* site_ref;     // by site id: a point on the mesh {x, y, z, 1} or {.., .., .., 0} = none
+    int no_seed;            // 1: d_min starts at +inf in the grouped scan too (P2M_NO_SEED)
     const uint32_t* grid_off;
     const uint32_t* grid_site;
     double grid_lo[3], grid_inv[3];

@@ -157,6 +157,7 @@ struct Slot {
     uint32_t *lf = nullptr, *bvh_perm = nullptr;
     uint8_t* heavy = nullptr;
     D4* site_pos = nullptr;
+    D4* site_ref = nullptr;
     uint32_t *grid_off = nullptr, *grid_site = nullptr;
     Params params{};
     std::mutex mu;
@@ -197,7 +198,7 @@ void free_slot(Slot& s) {
     cudaSetDevice(s.dev);
     cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
     cudaFree(s.heavy);
-    cudaFree(s.site_pos); cudaFree(s.grid_off); cudaFree(s.grid_site);
+    cudaFree(s.site_pos); cudaFree(s.site_ref); cudaFree(s.grid_off); cudaFree(s.grid_site);
     cudaFree(s.f32);
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
@@ -319,6 +320,7 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.agg, sizeof(unsigned long long) * 8));
     CK(cudaMalloc(&s.heavy, std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.site_pos, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMalloc(&s.site_ref, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     if (E.grid_cells) {
         CK(cudaMalloc(&s.grid_off, 4 * (E.grid_cells + 1)));
         CK(cudaMalloc(&s.grid_site, 4 * std::max<uint64_t>(1, E.grid_pairs)));
@@ -573,11 +575,21 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             for (int c = 0; c < 3; ++c) { P.grid_lo[c] = grid.lo[c]; P.grid_inv[c] = grid.inv[c]; P.grid_res[c] = grid.res[c]; }
         }
         if (std::getenv("P2M_NO_GRID")) E->grid_cells = E->grid_pairs = 0;
+        P.no_seed = std::getenv("P2M_NO_SEED") ? 1 : 0;
     }
-    std::vector<D4> site_pos(S);
-    for (uint64_t i = 0; i < S; ++i)
-        site_pos[i] = D4{d->site_xyz[3 * i], d->site_xyz[3 * i + 1], d->site_xyz[3 * i + 2],
-                         bits_to_double(d->site_kind[i] == P2M_SITE_SENTINEL ? (1ull << 34) : 0ull)};
+    std::vector<D4> site_pos(S), site_ref(S);
+    for (uint64_t i = 0; i < S; ++i) {
+        const double* x = d->site_xyz + 3 * i;
+        site_pos[i] = D4{x[0], x[1], x[2], bits_to_double(d->site_kind[i] == P2M_SITE_SENTINEL ? (1ull << 34) : 0ull)};
+        // a point on the mesh for the d_min seed: the vertex itself, or the auxiliary projection
+        site_ref[i] = D4{0.0, 0.0, 0.0, 0.0};
+        if (d->site_kind[i] == P2M_SITE_MESH_VERTEX) {
+            site_ref[i] = D4{x[0], x[1], x[2], 1.0};
+        } else if (d->site_kind[i] == P2M_SITE_AUXILIARY && d->site_ref_xyz) {
+            const double* r = d->site_ref_xyz + 3 * i;
+            if (std::isfinite(r[0]) && std::isfinite(r[1]) && std::isfinite(r[2])) site_ref[i] = D4{r[0], r[1], r[2], 1.0};
+        }
+    }
     // ---- upload to the first device, peer-replicate to the rest ----
     for (int k = 0; k < n_devices; ++k) {
         auto s = std::make_unique<Slot>();
@@ -601,13 +613,14 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.site_pos, site_pos.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.site_ref, site_ref.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
             (E->grid_cells && cudaMemcpy(s0.grid_off, grid.off.data(), 4 * (E->grid_cells + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
             (E->grid_pairs && cudaMemcpy(s0.grid_site, grid.site.data(), 4 * E->grid_pairs, cudaMemcpyHostToDevice) != cudaSuccess)) {
             set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
             return fail(P2M_ERR_CUDA);
         }
     }
-    E->bytes = sizeof(D4) * (2 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * F + 8 * (S + 1) + 4 * (L + F) + S +
+    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * F + 8 * (S + 1) + 4 * (L + F) + S +
                (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0);
     auto t0 = std::chrono::steady_clock::now();
     for (size_t k = 1; k < E->slots.size(); ++k) {
@@ -626,7 +639,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
             {s.off, s0.off, 8 * (S + 1)},
             {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
-            {s.site_pos, s0.site_pos, sizeof(D4) * S},
+            {s.site_pos, s0.site_pos, sizeof(D4) * S}, {s.site_ref, s0.site_ref, sizeof(D4) * S},
             {s.grid_off, s0.grid_off, E->grid_cells ? 4 * (E->grid_cells + 1) : 0},
             {s.grid_site, s0.grid_site, 4 * E->grid_pairs}};
         for (auto& c : cp)
@@ -645,6 +658,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.off = s->off; s->params.lf = s->lf;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
         s->params.site_pos = s->site_pos;
+        s->params.site_ref = s->site_ref;
         s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
         s->params.grid_site = s->grid_site;
     }

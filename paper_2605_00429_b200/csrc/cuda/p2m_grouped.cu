@@ -221,6 +221,19 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     const float finf = __int_as_float(0x7f800000);
     double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
     uint64_t DK = pk2(finf, finf);               // (dmin_up + delta) * K, rounded up, both halves
+    if (active && !p.no_seed) {
+        // Seed d_min with an upper bound of the distance to the mesh: |q - ref| for a point ref ON
+        // the mesh (the site itself for a mesh vertex, proj(s, M) for an auxiliary site).  A face
+        // whose lower bound exceeds it (plus the prune slack) cannot attain or tie the minimum, so
+        // the (d^2, face) argmin is unchanged; only exact evaluations are saved.  The sequential
+        // fused path keeps d_min = +inf (REF/SPEC.md:514) so its counters stay oracle-identical.
+        const D4 rf = ldg4(p.site_ref + s);
+        if (rf.w != 0.0) {
+            dmin = sqrt(vd2(q, V{rf.x, rf.y, rf.z}));
+            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+            DK = pk2(dkf, dkf);
+        }
+    }
     uint32_t bf = 0xffffffffu;
     uint32_t exact = 0;
     const uint64_t beg = p.off[s], end = p.off[s + 1];

@@ -91,6 +91,7 @@ P2M_API int p2m_host_engine_desc(const p2m_host_engine* he, p2m_engine_desc* d) 
         d->list_offsets = h.off.data();
         d->list_faces = h.lists.data();
         d->site_cell_box = h.cell_box.empty() ? nullptr : h.cell_box.data();
+        d->site_ref_xyz = h.refs.empty() ? nullptr : h.refs.data();
         d->domain_min[0] = h.D.lo.x; d->domain_min[1] = h.D.lo.y; d->domain_min[2] = h.D.lo.z;
         d->domain_max[0] = h.D.hi.x; d->domain_max[1] = h.D.hi.y; d->domain_max[2] = h.D.hi.z;
         return (int)P2M_OK;
