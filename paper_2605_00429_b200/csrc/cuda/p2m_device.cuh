@@ -89,6 +89,8 @@ struct Params {
     const D4* rec;          // 4 per face
     const float4* f32;      // per face fp32 pre-filter record: c rounded to nearest, r_up * K rounded up
     const uint64_t* off;    // S+1
+    const uint64_t* boff;   // S+1: first batch sphere of each list (one per aligned 32 entries)
+    const float4* bsph;     // batch spheres: centre rounded to nearest, radius (rounded up) * K
     const uint32_t* lf;     // list entries
     const D4* bvh;          // 2 per node
     const uint32_t* bvh_perm;  // leaf face ids
@@ -104,6 +106,7 @@ struct Params {
     const D4* site_pos;     // by site id: {x, y, z, meta (sentinel bit)}
     const D4* site_ref;     // by site id: a point on the mesh {x, y, z, 1} or {.., .., .., 0} = none
     int no_seed;            // 1: d_min starts at +inf in the grouped scan too (P2M_NO_SEED)
+    int no_batch;           // 1: no level-1 batch-sphere pruning (P2M_NO_BATCH)
     const uint32_t* grid_off;
     const uint32_t* grid_site;
     double grid_lo[3], grid_inv[3];

@@ -153,6 +153,8 @@ struct Slot {
     cudaStream_t stream = nullptr;
     D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
     float4* f32 = nullptr;
+    float4* bsph = nullptr;
+    uint64_t* boff = nullptr;
     uint64_t* off = nullptr;
     uint32_t *lf = nullptr, *bvh_perm = nullptr;
     uint8_t* heavy = nullptr;
@@ -190,6 +192,7 @@ struct p2m_engine {
     int e2e_chunks = 4;  // host-buffer path pipeline depth (P2M_E2E_CHUNKS overrides)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
+    uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
 };
 
 namespace {
@@ -200,6 +203,7 @@ void free_slot(Slot& s) {
     cudaFree(s.heavy);
     cudaFree(s.site_pos); cudaFree(s.site_ref); cudaFree(s.grid_off); cudaFree(s.grid_site);
     cudaFree(s.f32);
+    cudaFree(s.bsph); cudaFree(s.boff);
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
     }
@@ -313,6 +317,8 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.bsph, sizeof(float4) * std::max<uint64_t>(1, E.n_batches)));
+    CK(cudaMalloc(&s.boff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
     CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
@@ -526,6 +532,41 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
         f32[f] = make_float4((float)sp[0], (float)sp[1], (float)sp[2], rk);
     }
+    // level-1 pruning spheres: one per aligned 32-entry batch of every list.  Centre = centre of the
+    // members' sphere boxes; radius = max |c_i - C| + r_i, then made conservative for the fp32
+    // kernel test (centre rounded to nearest, radius grown by the centre's rounding and rounded up,
+    // times K rounded up -- the same form as the per-face records)
+    std::vector<uint64_t> boff(S + 1, 0);
+    for (uint64_t s = 0; s < S; ++s) boff[s + 1] = boff[s] + (d->list_offsets[s + 1] - d->list_offsets[s] + 31) / 32;
+    E->n_batches = boff[S];
+    std::vector<float4> bsph(std::max<uint64_t>(1, E->n_batches));
+    for (uint64_t s = 0; s < S; ++s) {
+        const uint64_t b0 = d->list_offsets[s], b1 = d->list_offsets[s + 1];
+        for (uint64_t j = b0, bi = boff[s]; j < b1; j += 32, ++bi) {
+            const uint64_t je = std::min(b1, j + 32);
+            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (uint64_t t = j; t < je; ++t) {
+                const double* sp = d->face_sphere + 4 * (uint64_t)d->list_faces[t];
+                for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], sp[k] - sp[3]); hi[k] = std::max(hi[k], sp[k] + sp[3]); }
+            }
+            double C[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+            float cf[3] = {(float)C[0], (float)C[1], (float)C[2]};
+            double R = 0.0;
+            for (uint64_t t = j; t < je; ++t) {
+                const double* sp = d->face_sphere + 4 * (uint64_t)d->list_faces[t];
+                double dd = 0.0;
+                for (int k = 0; k < 3; ++k) dd += (sp[k] - (double)cf[k]) * (sp[k] - (double)cf[k]);
+                R = std::max(R, std::sqrt(dd) + sp[3]);
+            }
+            R = R * (1.0 + 1e-12) + 1e-300;
+            float rf = (float)R;
+            if ((double)rf < R) rf = std::nextafter(rf, INFINITY);
+            const double prod = (double)rf * (double)1.000001f;
+            float rk = (float)prod;
+            if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
+            bsph[bi] = make_float4(cf[0], cf[1], cf[2], rk);
+        }
+    }
     FlatBvh bvh;
     build_bvh(d->tri_xyz, F, bvh);
     E->n_bvh = bvh.nodes.size() / 2;
@@ -576,6 +617,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         }
         if (std::getenv("P2M_NO_GRID")) E->grid_cells = E->grid_pairs = 0;
         P.no_seed = std::getenv("P2M_NO_SEED") ? 1 : 0;
+        P.no_batch = std::getenv("P2M_NO_BATCH") ? 1 : 0;
     }
     std::vector<D4> site_pos(S), site_ref(S);
     for (uint64_t i = 0; i < S; ++i) {
@@ -608,6 +650,8 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         if (cudaMemcpy(s0.kd, kd.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.rec, rec.data(), sizeof(D4) * 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.f32, f32.data(), sizeof(float4) * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.bsph, bsph.data(), sizeof(float4) * bsph.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.boff, boff.data(), 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
             cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -620,7 +664,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             return fail(P2M_ERR_CUDA);
         }
     }
-    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * F + 8 * (S + 1) + 4 * (L + F) + S +
+    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (F + E->n_batches) + 8 * (S + 1) + 8 * (S + 1) + 4 * (L + F) + S +
                (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0);
     auto t0 = std::chrono::steady_clock::now();
     for (size_t k = 1; k < E->slots.size(); ++k) {
@@ -637,6 +681,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         }
         struct { void* dst; const void* src; size_t n; } cp[] = {
             {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
+            {s.bsph, s0.bsph, sizeof(float4) * std::max<uint64_t>(1, E->n_batches)}, {s.boff, s0.boff, 8 * (S + 1)},
             {s.off, s0.off, 8 * (S + 1)},
             {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
             {s.site_pos, s0.site_pos, sizeof(D4) * S}, {s.site_ref, s0.site_ref, sizeof(D4) * S},
@@ -655,7 +700,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto& s : E->slots) {
         s->params = P;
-        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.off = s->off; s->params.lf = s->lf;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
         s->params.site_pos = s->site_pos;
         s->params.site_ref = s->site_ref;

@@ -190,6 +190,8 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
     __shared__ D4 s_tri[kChunk * 3];             // the chunk's triangles (96 B each) for the rare path
+    __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
+    __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
     __shared__ double s_rd[kTile];
     __shared__ uint32_t s_rf[kTile];
     __shared__ uint32_t s_re[kTile];
@@ -242,14 +244,43 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     uint32_t nf = 0;
     float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
     if (beg + tid < end) { nf = p.lf[beg + tid]; nv = p.f32[nf]; }
+    const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
     for (uint64_t base = beg; base < end; base += kChunk) {
         const int mc = (int)min((uint64_t)kChunk, end - base);
+        const int nb = (mc + 31) >> 5;
         if (base != beg) __syncthreads();        // the previous chunk is fully consumed
+        // level 1: the enclosing sphere of each 32-entry batch.  If every lane's conservative fp32
+        // bound to it exceeds the lane's d_min, every member sphere's bound does too, so the whole
+        // batch is pruned exactly as the per-candidate tests would prune it (and is never staged).
+        if (tid < nb) s_bsph[tid] = p.bsph[bo + ((base - beg) >> 5) + tid];
+        if (tid == 0) s_need = 0u;
+        __syncthreads();
+        uint32_t wneed = 0;
+        if (warp_on) {
+            for (int bb = r; bb < nb; bb += R) {
+                bool need = p.no_batch != 0;
+                if (active && !need) {
+                    const float4 c = s_bsph[bb];
+                    float dkx, dky;
+                    upk2(DK, dkx, dky);
+                    const float dx = __uint_as_float((uint32_t)QX) - c.x;
+                    const float dy = __uint_as_float((uint32_t)QY) - c.y;
+                    const float dz = __uint_as_float((uint32_t)QZ) - c.z;
+                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                    const float th = __fadd_ru(c.w, dkx);
+                    need = !(d2f > __fmul_ru(th, th));
+                }
+                if (__any_sync(0xffffffffu, need)) wneed |= 1u << bb;
+            }
+            if (lane == 0 && wneed) atomicOr(&s_need, wneed);
+        }
+        __syncthreads();
+        const uint32_t cneed = s_need;
         {
             const int pp = tid >> 1, h = tid & 1;
             if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
             s_fid[tid] = nf;
-            if (tid < mc) {  // stage the triangle: the rare path then reads broadcast shared memory
+            if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the triangle: the rare path then reads broadcast shared memory
                 const D4* rec = p.rec + 4 * (uint64_t)nf;
                 s_tri[3 * tid] = ldg4(rec + 1);
                 s_tri[3 * tid + 1] = ldg4(rec + 2);
@@ -265,8 +296,8 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
         const uint64_t nxt = base + kChunk + tid;
         if (nxt < end) { nf = p.lf[nxt]; nv = p.f32[nf]; }
         if (!warp_on) continue;
-        const int nb = (mc + 31) >> 5;
         for (int bb = r; bb < nb; bb += R) {
+            if (!((wneed >> bb) & 1u)) continue;  // pruned whole by its batch sphere
             const int k0 = bb * 32;
             uint32_t mask = 0;
             if (active) {
