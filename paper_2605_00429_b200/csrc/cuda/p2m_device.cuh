@@ -88,6 +88,9 @@ struct Params {
     uint32_t n_nodes;
     const D4* rec;          // 4 per face
     const float4* f32;      // per face fp32 pre-filter record: c rounded to nearest, r_up * K rounded up
+    const float4* lbr;      // per face 4 x float4: a, unit normal n, in-plane outward edge normals m_ab,
+                            // m_bc, m_ca, offset m_bc.(b-a) -- the tight lower bound sqrt(h^2+max(0,s_i)^2)
+    float lb_margin;        // absolute fp32 error bound of that lower bound (64 * 2^-24 * M)
     const uint64_t* off;    // S+1
     const uint64_t* boff;   // S+1: first batch sphere of each list (one per aligned 32 entries)
     const float4* bsph;     // batch spheres: centre rounded to nearest, radius (rounded up) * K

@@ -154,6 +154,7 @@ struct Slot {
     D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
     float4* f32 = nullptr;
     float4* bsph = nullptr;
+    float4* lbr = nullptr;
     uint64_t* boff = nullptr;
     uint64_t* off = nullptr;
     uint32_t *lf = nullptr, *bvh_perm = nullptr;
@@ -203,7 +204,7 @@ void free_slot(Slot& s) {
     cudaFree(s.heavy);
     cudaFree(s.site_pos); cudaFree(s.site_ref); cudaFree(s.grid_off); cudaFree(s.grid_site);
     cudaFree(s.f32);
-    cudaFree(s.bsph); cudaFree(s.boff);
+    cudaFree(s.bsph); cudaFree(s.boff); cudaFree(s.lbr);
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
     }
@@ -318,6 +319,7 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.bsph, sizeof(float4) * std::max<uint64_t>(1, E.n_batches)));
+    CK(cudaMalloc(&s.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.boff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
@@ -518,7 +520,17 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         rec[4 * f] = D4{s[0], s[1], s[2], s[3]};
         rec[4 * f + 1] = D4{t[0], t[1], t[2], t[3]};
         rec[4 * f + 2] = D4{t[4], t[5], t[6], t[7]};
-        rec[4 * f + 3] = D4{t[8], 0.0, 0.0, 0.0};
+        // padding of the last sector: the face's unit normal in fp32 (for the plane-distance bound)
+        const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+        const double vx = t[6] - t[0], vy = t[7] - t[1], vz = t[8] - t[2];
+        double nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
+        const double nl = std::sqrt(nx * nx + ny * ny + nz * nz);
+        if (nl > 0.0 && std::isfinite(nl)) { nx /= nl; ny /= nl; nz /= nl; } else { nx = ny = nz = 0.0; }
+        const float fn[4] = {(float)nx, (float)ny, (float)nz, 0.0f};
+        double p0, p1;
+        std::memcpy(&p0, fn, 8);
+        std::memcpy(&p1, fn + 2, 8);
+        rec[4 * f + 3] = D4{t[8], p0, p1, 0.0};
     }
     // fp32 pre-filter records (k_scan_tiles): centre rounded to nearest, radius rounded up and
     // multiplied by K = 1.000001 rounding up -- the same values the kernel's bound assumes
@@ -567,6 +579,35 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             bsph[bi] = make_float4(cf[0], cf[1], cf[2], rk);
         }
     }
+    // tight fp32 lower-bound records (k_scan_tiles rare path): d(q,T)^2 >= h^2 + max(0, s_i)^2 with
+    // h = n.(q-a) and s_i the signed in-plane distances to the three edge lines (outward positive)
+    std::vector<float4> lbr(4 * std::max<uint64_t>(1, F));
+    for (uint64_t f = 0; f < F; ++f) {
+        const double* t = d->tri_xyz + 9 * f;
+        const double A[3] = {t[0], t[1], t[2]}, B[3] = {t[3], t[4], t[5]}, Cc[3] = {t[6], t[7], t[8]};
+        auto sub3 = [](const double* x, const double* y, double* o) { for (int k = 0; k < 3; ++k) o[k] = x[k] - y[k]; };
+        auto crs = [](const double* x, const double* y, double* o) {
+            o[0] = x[1] * y[2] - x[2] * y[1]; o[1] = x[2] * y[0] - x[0] * y[2]; o[2] = x[0] * y[1] - x[1] * y[0];
+        };
+        auto unit = [](double* v) {
+            const double l = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            if (l > 0.0 && std::isfinite(l)) { v[0] /= l; v[1] /= l; v[2] /= l; return true; }
+            v[0] = v[1] = v[2] = 0.0;
+            return false;
+        };
+        double ab[3], ac[3], bc[3], ca[3], n[3], m1[3], m2[3], m3[3];
+        sub3(B, A, ab); sub3(Cc, A, ac); sub3(Cc, B, bc); sub3(A, Cc, ca);
+        crs(ab, ac, n);
+        bool ok = unit(n);
+        crs(ab, n, m1); crs(bc, n, m2); crs(ca, n, m3);
+        ok = ok && unit(m1) && unit(m2) && unit(m3);
+        if (!ok) { for (int k = 0; k < 3; ++k) n[k] = m1[k] = m2[k] = m3[k] = 0.0; }  // never prunes
+        const double o2 = ok ? (m2[0] * ab[0] + m2[1] * ab[1] + m2[2] * ab[2]) : 0.0;
+        lbr[4 * f] = make_float4((float)A[0], (float)A[1], (float)A[2], (float)n[0]);
+        lbr[4 * f + 1] = make_float4((float)n[1], (float)n[2], (float)m1[0], (float)m1[1]);
+        lbr[4 * f + 2] = make_float4((float)m1[2], (float)m2[0], (float)m2[1], (float)m2[2]);
+        lbr[4 * f + 3] = make_float4((float)m3[0], (float)m3[1], (float)m3[2], (float)o2);
+    }
     FlatBvh bvh;
     build_bvh(d->tri_xyz, F, bvh);
     E->n_bvh = bvh.nodes.size() / 2;
@@ -590,6 +631,12 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         float df = (float)delta;
         if ((double)df < delta) df = std::nextafter(df, INFINITY);
         P.f32_delta = df;
+        // lower-bound record error: each dot product of a unit vector with fl(q_f - a_f) is within
+        // ~25*2^-24*M of exact, the edge offset adds ~4*2^-24*M; 64*2^-24*M covers both with margin
+        const double lm = 64.0 * std::ldexp(1.0, -24) * M;
+        float lmf = (float)lm;
+        if ((double)lmf < lm) lmf = std::nextafter(lmf, INFINITY);
+        P.lb_margin = lmf;
     }
     P.long_tile = 32;
     if (const char* v = std::getenv("P2M_LONG_TILE")) {
@@ -652,6 +699,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             cudaMemcpy(s0.f32, f32.data(), sizeof(float4) * F, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.bsph, bsph.data(), sizeof(float4) * bsph.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.boff, boff.data(), 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.lbr, lbr.data(), sizeof(float4) * lbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
             cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -664,7 +712,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             return fail(P2M_ERR_CUDA);
         }
     }
-    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (F + E->n_batches) + 8 * (S + 1) + 8 * (S + 1) + 4 * (L + F) + S +
+    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (5 * F + E->n_batches) + 8 * (S + 1) + 8 * (S + 1) + 4 * (L + F) + S +
                (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0);
     auto t0 = std::chrono::steady_clock::now();
     for (size_t k = 1; k < E->slots.size(); ++k) {
@@ -682,6 +730,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         struct { void* dst; const void* src; size_t n; } cp[] = {
             {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
             {s.bsph, s0.bsph, sizeof(float4) * std::max<uint64_t>(1, E->n_batches)}, {s.boff, s0.boff, 8 * (S + 1)},
+            {s.lbr, s0.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, F)},
             {s.off, s0.off, 8 * (S + 1)},
             {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
             {s.site_pos, s0.site_pos, sizeof(D4) * S}, {s.site_ref, s0.site_ref, sizeof(D4) * S},
@@ -700,7 +749,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto& s : E->slots) {
         s->params = P;
-        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.lbr = s->lbr; s->params.off = s->off; s->params.lf = s->lf;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
         s->params.site_pos = s->site_pos;
         s->params.site_ref = s->site_ref;

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                                                          const uint32_t* __restrict__ meta, Out o) {
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
-    __shared__ D4 s_tri[kChunk * 3];             // the chunk's triangles (96 B each) for the rare path
+    __shared__ float4 s_lb[kChunk * 4];          // the chunk's fp32 lower-bound records (64 B each)
     __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
     __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
     __shared__ double s_rd[kTile];
@@ -245,6 +245,28 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
     if (beg + tid < end) { nf = p.lf[beg + tid]; nv = p.f32[nf]; }
     const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
+    if (active && !p.no_seed && !p.no_batch) {
+        // Tighter seed: every face of batch b lies within |q - C_b| + R_b of q, so the min of that over
+        // the list's batch spheres bounds the distance to the mesh from above.  fp32 with upward
+        // rounding: sqrt(d2f)*(1+1e-6) covers the rounding of d2f, delta the fp32 rounding of q
+        // (C_b is an exact float), and the stored radius is R*K rounded up (>= R).
+        const uint64_t nbl = p.boff[s + 1] - bo;
+        float ub = __int_as_float(0x7f800000);
+        const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY),
+                    qzf = __uint_as_float((uint32_t)QZ);
+        for (uint64_t b2 = 0; b2 < nbl; ++b2) {
+            const float4 c = p.bsph[bo + b2];  // same address across the tile's lanes: broadcast
+            const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+            ub = fminf(ub, __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w));
+        }
+        ub = __fadd_ru(ub, delta);
+        if ((double)ub < dmin) {
+            dmin = (double)ub;
+            const float dkf = __fmul_ru(__fadd_ru(ub, delta), K);
+            DK = pk2(dkf, dkf);
+        }
+    }
     for (uint64_t base = beg; base < end; base += kChunk) {
         const int mc = (int)min((uint64_t)kChunk, end - base);
         const int nb = (mc + 31) >> 5;
@@ -280,11 +302,12 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
             const int pp = tid >> 1, h = tid & 1;
             if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
             s_fid[tid] = nf;
-            if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the triangle: the rare path then reads broadcast shared memory
-                const D4* rec = p.rec + 4 * (uint64_t)nf;
-                s_tri[3 * tid] = ldg4(rec + 1);
-                s_tri[3 * tid + 1] = ldg4(rec + 2);
-                s_tri[3 * tid + 2] = ldg4(rec + 3);
+            if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the lower-bound record (rare path, broadcast)
+                const float4* lr = p.lbr + 4 * (uint64_t)nf;
+                s_lb[4 * tid] = lr[0];
+                s_lb[4 * tid + 1] = lr[1];
+                s_lb[4 * tid + 2] = lr[2];
+                s_lb[4 * tid + 3] = lr[3];
             }
             s_pf[8 * pp + h] = nv.x;
             s_pf[8 * pp + 2 + h] = nv.y;
@@ -343,9 +366,31 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                         if (d2f > __fmul_ru(th, th)) continue;
                     }
                     const uint32_t f = s_fid[k0 + kk];
-                    const D4 t0 = s_tri[3 * (k0 + kk)], t1 = s_tri[3 * (k0 + kk) + 1], t2 = s_tri[3 * (k0 + kk) + 2];
-                    V pp3;
-                    const double dd = closest_tri(q, V{t0.x, t0.y, t0.z}, V{t0.w, t1.x, t1.y}, V{t1.z, t1.w, t2.x}, &pp3);
+                    {
+                        // tight lower bound d(q,T)^2 >= h^2 + max(0, s_ab, s_bc, s_ca)^2: h the distance
+                        // to the supporting plane, s_i the signed in-plane distances to the edge lines
+                        // (the triangle is the intersection of the three half-planes).  fp32 error is at
+                        // most p.lb_margin; skip iff lb > (d_min + delta)*K + margin (>= d_min + 2 eps +
+                        // error): the face can neither beat nor tie the running minimum.
+                        const float4 r0 = s_lb[4 * (k0 + kk)], r1 = s_lb[4 * (k0 + kk) + 1];
+                        const float4 r2 = s_lb[4 * (k0 + kk) + 2], r3 = s_lb[4 * (k0 + kk) + 3];
+                        const float dx = __uint_as_float((uint32_t)QX) - r0.x;
+                        const float dy = __uint_as_float((uint32_t)QY) - r0.y;
+                        const float dz = __uint_as_float((uint32_t)QZ) - r0.z;
+                        const float hh = __fmaf_rn(r0.w, dx, __fmaf_rn(r1.x, dy, __fmul_rn(r1.y, dz)));
+                        const float s1 = __fmaf_rn(r1.z, dx, __fmaf_rn(r1.w, dy, __fmul_rn(r2.x, dz)));
+                        const float s2 = __fmaf_rn(r2.y, dx, __fmaf_rn(r2.z, dy, __fmul_rn(r2.w, dz))) - r3.w;
+                        const float s3 = __fmaf_rn(r3.x, dx, __fmaf_rn(r3.y, dy, __fmul_rn(r3.z, dz)));
+                        const float ee = fmaxf(0.f, fmaxf(s1, fmaxf(s2, s3)));
+                        const float lb2 = __fmaf_rn(hh, hh, __fmul_rn(ee, ee));
+                        float dkx, dky;
+                        upk2(DK, dkx, dky);
+                        const float th = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
+                        if (lb2 > __fmul_ru(th, th)) continue;
+                    }
+                    V a, bb3, c3, pp3;
+                    load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
+                    const double dd = closest_tri(q, a, bb3, c3, &pp3);
                     ++exact;
                     if (dd < best || (dd == best && f < bf)) {
                         best = dd;
