@@ -1,13 +1,6 @@
-python -m pytest tests/test_gpu_parity.py -q -m "gpu and not slow" 2>&1 | grep -E "passed|failed|Error|assert" | tail -6
-for cfg in 1 2; do
-python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/q_${cfg}.json 2>gpurun_out/q.err
+for ch in 2 4 6 8 12; do
+P2M_E2E_CHUNKS=$ch python bench.py --config 2 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 5 > gpurun_out/q_ch$ch.json 2>gpurun_out/q.err
 python -c "
-import json; d=json.load(open('gpurun_out/q_${cfg}.json')); s=d['config']['split_ms']; pq=d['config']['per_query']
-print('c$cfg', round(d['value']/1e6,1), 'Mq/s', {k: round(v,2) for k,v in s.items()}, 'E/q', round(pq['exact'],1), 'e2e', round(d['e2e']['value']/1e6,1))"
-done
-for cfg in 5; do
-python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 1 --queries 10000000 > gpurun_out/q_${cfg}.json 2>gpurun_out/q.err
-python -c "
-import json; d=json.load(open('gpurun_out/q_${cfg}.json')); s=d['config']['split_ms']; pq=d['config']['per_query']
-print('c$cfg (10M)', round(d['value']/1e6,1), 'Mq/s', {k: round(v,2) for k,v in s.items()}, 'E/q', round(pq['exact'],1), 'e2e', round(d['e2e']['value']/1e6,1))"
+import json; d=json.load(open('gpurun_out/q_ch$ch.json'))
+print('chunks $ch', round(d['value']/1e6,1), 'Mq/s e2e', round(d['e2e']['value']/1e6,1))"
 done

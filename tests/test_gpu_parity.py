@@ -223,3 +223,42 @@ def test_grid_and_kdtree_locate_agree(c2):
         assert getattr(r_grid, k).tobytes() == getattr(r_kd, k).tobytes(), k
     ref = O.OracleEngine(h.arrays()).batch_query(q)
     _compare(r_grid, ref, len(q))
+
+
+def _surface_probes(V, F, n, rng, scales):
+    """Points on faces, at vertices and on edges, pushed off the surface by tiny normal offsets --
+    the regime where the fp32 pre-filters run closest to their margins."""
+    t = F[rng.integers(0, len(F), n)]
+    a, b, c = V[t[:, 0]], V[t[:, 1]], V[t[:, 2]]
+    w = rng.dirichlet([1, 1, 1], size=n)
+    kind = rng.integers(0, 3, n)
+    w[kind == 1] = [1.0, 0.0, 0.0]                      # vertices
+    w[kind == 2] = np.c_[rng.uniform(size=(kind == 2).sum()), np.zeros(((kind == 2).sum(), 1)), np.zeros(((kind == 2).sum(), 1))]
+    w[kind == 2, 1] = 1.0 - w[kind == 2, 0]             # edges ab
+    p = w[:, :1] * a + w[:, 1:2] * b + w[:, 2:3] * c
+    nrm = np.cross(b - a, c - a)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    off = rng.choice(scales, size=n) * rng.choice([-1.0, 1.0], size=n)
+    return p + nrm * off[:, None]
+
+
+@pytest.mark.parametrize("variant", ["far_translated", "slivers"])
+def test_fp32_prefilters_stress(variant):
+    rng = np.random.default_rng(17)
+    V, F = P.icosphere(3)
+    if variant == "far_translated":
+        V = V * 1e3 + np.array([5e3, -2e3, 1e3])       # large |coordinates| vs feature size
+        scale = 1e3
+    else:
+        V = V * (1.0 + 0.15 * rng.standard_normal((len(V), 1)))  # bumpy: thin and obtuse faces
+        V[::7] += 0.02 * rng.standard_normal((len(V[::7]), 3))
+        scale = 1.0
+    h = P.HostEngine.build(V, F)
+    Vv, Ff = h.mesh()
+    q = np.concatenate([
+        _surface_probes(Vv, Ff, 60_000, rng, np.array([0.0, 1e-12, 1e-9, 1e-6, 1e-4, 1e-2]) * scale),
+        Vv.mean(0) + rng.uniform(-1.3, 1.3, size=(40_000, 3)) * scale,
+    ])
+    r = P.Engine(h).batch_query(q)
+    ref = O.OracleEngine(h.arrays()).batch_query(q)
+    _compare(r, ref, len(q))
