@@ -166,8 +166,8 @@ struct Slot {
     std::mutex mu;
     // host-API path: kPipe streams, each with a chunk-sized staging set, so the H2D copy of one
     // chunk, the kernels of another and the D2H copy of a third overlap
-    static constexpr int kPipe = 3;
-    cudaStream_t pipe[kPipe] = {nullptr, nullptr, nullptr};
+    static constexpr int kPipe = 4;
+    cudaStream_t pipe[kPipe] = {};
     struct Ws {
         double *q = nullptr, *dist = nullptr, *cp = nullptr;
         uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;

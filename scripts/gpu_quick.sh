@@ -1,4 +1,4 @@
-for ch in 2 3 4 5; do
+for ch in 4 6 8; do
 P2M_E2E_CHUNKS=$ch python bench.py --config 2 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 5 > gpurun_out/q_ch$ch.json 2>gpurun_out/q.err
 python -c "
 import json; d=json.load(open('gpurun_out/q_ch$ch.json'))
