@@ -373,7 +373,8 @@ def main():
             "build": tb, "n_sites": st["n_sites"], "n_faces": st["n_faces"], "list_avg": st["list_avg"],
             "list_max": st["list_max"],
             "per_query": {"candidates": c["candidates_visited"] / n, "exact": c["exact_evaluations"] / n,
-                          "kd_nodes": c["kd_nodes_visited"] / n, "fallbacks": c["fallbacks"]},
+                          "kd_nodes": c["kd_nodes_visited"] / n, "fallbacks": c["fallbacks"],
+                          "filter_passes": c["filter_passes"] / n, "warp_rare_iters": c["warp_rare_iters"] / n},
             "split_ms": {"morton": split[0], "sort": split[1], "descend": split[2], "regroup_sort": split[3], "scan": split[4], "total": split[5]},
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

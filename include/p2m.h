@@ -86,7 +86,9 @@ typedef struct p2m_counters {
     uint64_t exact_evaluations;  /* point-triangle evaluations after sphere pruning */
     uint64_t pruned;             /* candidates_visited - exact_evaluations */
     uint64_t fallbacks;          /* rows answered by the BVH fallback */
-    uint64_t kd_nodes_visited;   /* nearest-site tree nodes whose distance was evaluated */
+    uint64_t kd_nodes_visited;   /* nearest-site candidates evaluated (k-d nodes or grid candidates) */
+    uint64_t filter_passes;      /* grouped scan: candidates passing the first fp32 sphere test (diag.) */
+    uint64_t warp_rare_iters;    /* grouped scan: warp-level rare-path iterations x 32 (diagnostic) */
 } p2m_counters;
 
 typedef struct p2m_engine p2m_engine;

@@ -55,6 +55,8 @@ class Counters(C.Structure):
         ("pruned", C.c_uint64),
         ("fallbacks", C.c_uint64),
         ("kd_nodes_visited", C.c_uint64),
+        ("filter_passes", C.c_uint64),
+        ("warp_rare_iters", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -807,6 +807,8 @@ P2M_API int p2m_query_device(p2m_engine* e, int slot, const double* d_q, uint64_
         cnt->exact_evaluations = h[1];
         cnt->pruned = h[0] - h[1];
         cnt->kd_nodes_visited = h[2];
+        cnt->filter_passes = h[4];
+        cnt->warp_rare_iters = h[5];
         cnt->fallbacks = h[3];
     }
     return P2M_OK;
@@ -890,6 +892,8 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             parts[g].exact_evaluations = h[1];
             parts[g].pruned = h[0] - h[1];
             parts[g].kd_nodes_visited = h[2];
+            parts[g].filter_passes = h[4];
+            parts[g].warp_rare_iters = h[5];
             parts[g].fallbacks = h[3];
             return P2M_OK;
         };
@@ -912,6 +916,8 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             cnt->exact_evaluations += c.exact_evaluations;
             cnt->pruned += c.pruned;
             cnt->kd_nodes_visited += c.kd_nodes_visited;
+            cnt->filter_passes += c.filter_passes;
+            cnt->warp_rare_iters += c.warp_rare_iters;
             cnt->fallbacks += c.fallbacks;
         }
     }

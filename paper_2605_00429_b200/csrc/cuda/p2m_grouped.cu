@@ -168,6 +168,20 @@ __device__ __forceinline__ uint64_t mul2_up(uint64_t a, uint64_t b) {
     return r;
 }
 
+// Tight lower bound of d(q, T)^2 from a staged 64-byte record (a, n, m_ab, m_bc, m_ca, o_bc):
+// h^2 + max(0, s_ab, s_bc, s_ca)^2 with h = n.(q-a) and s_i the signed in-plane edge-line distances
+// (the triangle is the intersection of three half-planes).  fp32 error <= Params::lb_margin.
+__device__ __forceinline__ float lb2_face(const float4* r, float qx, float qy, float qz) {
+    const float4 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3];
+    const float dx = qx - r0.x, dy = qy - r0.y, dz = qz - r0.z;
+    const float hh = __fmaf_rn(r0.w, dx, __fmaf_rn(r1.x, dy, __fmul_rn(r1.y, dz)));
+    const float s1 = __fmaf_rn(r1.z, dx, __fmaf_rn(r1.w, dy, __fmul_rn(r2.x, dz)));
+    const float s2 = __fmaf_rn(r2.y, dx, __fmaf_rn(r2.z, dy, __fmul_rn(r2.w, dz))) - r3.w;
+    const float s3 = __fmaf_rn(r3.x, dx, __fmaf_rn(r3.y, dy, __fmul_rn(r3.z, dz)));
+    const float ee = fmaxf(0.f, fmaxf(s1, fmaxf(s2, s3)));
+    return __fmaf_rn(hh, hh, __fmul_rn(ee, ee));
+}
+
 // One CTA per tile (all rows share one site).  A tile of m rows uses G = ceil(m/32) warps per
 // replica and R = 8 / G replicas; replica r scans the 32-candidate batches b == r (mod R) of every
 // staged chunk, so small groups still keep all 8 warps busy.  Per batch, each lane computes a
@@ -238,6 +252,7 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     }
     uint32_t bf = 0xffffffffu;
     uint32_t exact = 0;
+    unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     float* s_pf = reinterpret_cast<float*>(s_pair);
     // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
@@ -343,17 +358,13 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                 if (valid < 32) mask &= (1u << valid) - 1u;
             }
             uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+            if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
             while (um) {
                 const int kk = __ffs(um) - 1;
                 um &= um - 1;
                 if ((mask >> kk) & 1u) {
-                    // The conservative fp32 test above already pruned everything the oracle's fp64
-                    // sphere test would prune except a sliver within its margin; re-testing in fp64
-                    // would cost a dependent 32-byte load and ~15 DP ops per survivor, while
-                    // evaluating a few extra candidates exactly can never change the minimum.  (The
-                    // fused path keeps the fp64 test, so its counters match the oracle exactly.)
                     // the batch mask used the d_min of the batch start: re-test this candidate with
-                    // the current one (same conservative fp32 test, operands already in smem)
+                    // the current one (same conservative fp32 sphere test, operands already in smem)
                     {
                         const int k = k0 + kk, pp = k >> 1, h = k & 1;
                         float dkx, dky;
@@ -364,30 +375,13 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                         const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
                         const float th = __fadd_ru(s_pf[8 * pp + 6 + h], dkx);
                         if (d2f > __fmul_ru(th, th)) continue;
+                        // then the tight lower bound
+                        const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
+                        if (lb2_face(s_lb + 4 * k, __uint_as_float((uint32_t)QX), __uint_as_float((uint32_t)QY),
+                                     __uint_as_float((uint32_t)QZ)) > __fmul_ru(thl, thl))
+                            continue;
                     }
                     const uint32_t f = s_fid[k0 + kk];
-                    {
-                        // tight lower bound d(q,T)^2 >= h^2 + max(0, s_ab, s_bc, s_ca)^2: h the distance
-                        // to the supporting plane, s_i the signed in-plane distances to the edge lines
-                        // (the triangle is the intersection of the three half-planes).  fp32 error is at
-                        // most p.lb_margin; skip iff lb > (d_min + delta)*K + margin (>= d_min + 2 eps +
-                        // error): the face can neither beat nor tie the running minimum.
-                        const float4 r0 = s_lb[4 * (k0 + kk)], r1 = s_lb[4 * (k0 + kk) + 1];
-                        const float4 r2 = s_lb[4 * (k0 + kk) + 2], r3 = s_lb[4 * (k0 + kk) + 3];
-                        const float dx = __uint_as_float((uint32_t)QX) - r0.x;
-                        const float dy = __uint_as_float((uint32_t)QY) - r0.y;
-                        const float dz = __uint_as_float((uint32_t)QZ) - r0.z;
-                        const float hh = __fmaf_rn(r0.w, dx, __fmaf_rn(r1.x, dy, __fmul_rn(r1.y, dz)));
-                        const float s1 = __fmaf_rn(r1.z, dx, __fmaf_rn(r1.w, dy, __fmul_rn(r2.x, dz)));
-                        const float s2 = __fmaf_rn(r2.y, dx, __fmaf_rn(r2.z, dy, __fmul_rn(r2.w, dz))) - r3.w;
-                        const float s3 = __fmaf_rn(r3.x, dx, __fmaf_rn(r3.y, dy, __fmul_rn(r3.z, dz)));
-                        const float ee = fmaxf(0.f, fmaxf(s1, fmaxf(s2, s3)));
-                        const float lb2 = __fmaf_rn(hh, hh, __fmul_rn(ee, ee));
-                        float dkx, dky;
-                        upk2(DK, dkx, dky);
-                        const float th = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-                        if (lb2 > __fmul_ru(th, th)) continue;
-                    }
                     V a, bb3, c3, pp3;
                     load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
                     const double dd = closest_tri(q, a, bb3, c3, &pp3);
@@ -439,6 +433,16 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     }
     if (kCounters && o.agg) {
         unsigned long long v0 = writer ? (end - beg) : 0ull, v1 = writer ? exact : 0u;
+        unsigned long long v2 = passes, v3 = rare_iters;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            v2 += __shfl_down_sync(0xffffffffu, v2, sh);
+            v3 += __shfl_down_sync(0xffffffffu, v3, sh);
+        }
+        if (lane == 0) {
+            atomicAdd(o.agg + 4, v2);
+            atomicAdd(o.agg + 5, v3);
+        }
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) {
             v0 += __shfl_down_sync(0xffffffffu, v0, sh);

@@ -1,6 +1,6 @@
-for ch in 4 6 8; do
-P2M_E2E_CHUNKS=$ch python bench.py --config 2 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 5 > gpurun_out/q_ch$ch.json 2>gpurun_out/q.err
+for cfg in 1 2; do
+python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/q_${cfg}.json 2>gpurun_out/q.err
 python -c "
-import json; d=json.load(open('gpurun_out/q_ch$ch.json'))
-print('chunks $ch', round(d['value']/1e6,1), 'Mq/s e2e', round(d['e2e']['value']/1e6,1))"
+import json; d=json.load(open('gpurun_out/q_${cfg}.json')); s=d['config']['split_ms']; pq=d['config']['per_query']
+print('c$cfg', round(d['value']/1e6,1), 'Mq/s', {k: round(v,2) for k,v in s.items()}, {k: round(v,1) for k, v in pq.items()}, 'e2e', round(d['e2e']['value']/1e6,1))"
 done
