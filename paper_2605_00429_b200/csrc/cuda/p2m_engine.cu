@@ -643,20 +643,22 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         uint32_t t = (uint32_t)std::strtoul(v, nullptr, 10);
         if (t == 32 || t == 64 || t == 128 || t == 256) P.long_tile = t;
     }
+    double kext[3] = {0, 0, 0};  // Morton key box = cell-locate grid box extents
     for (int c = 0; c < 3; ++c) {
         P.dmin[c] = d->domain_min[c];
         P.dmax[c] = d->domain_max[c];
         if (!(klo[c] <= khi[c])) { klo[c] = d->domain_min[c]; khi[c] = d->domain_max[c]; }
-        double mid = 0.5 * (klo[c] + khi[c]), h = 0.75 * (khi[c] - klo[c]);
+        double mid = 0.5 * (klo[c] + khi[c]), h = 0.75 * (khi[c] - klo[c]);  // = builder.cpp gbox
         if (!(h > 0)) h = 1.0;
         P.key_lo[c] = mid - h;
         P.key_scale[c] = 1024.0 / (2.0 * h);
+        kext[c] = 2.0 * h;
     }
 
     Grid grid;
     {
         double ext[3];
-        for (int c = 0; c < 3; ++c) ext[c] = 1024.0 / P.key_scale[c];
+        for (int c = 0; c < 3; ++c) ext[c] = kext[c];
         if (build_grid(d, P.key_lo, ext, grid)) {
             E->grid_cells = (uint64_t)grid.res[0] * grid.res[1] * grid.res[2];
             E->grid_pairs = grid.site.size();

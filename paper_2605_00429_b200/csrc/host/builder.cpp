@@ -316,6 +316,23 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
     const uint64_t S = h.sites.size();
     std::vector<std::vector<uint32_t>> per(S);
     h.cell_box.assign(6 * S, std::nan(""));
+    // the device's grid box (p2m_engine.cu: 1.5x the real sites' AABB about its centre, a flat axis
+    // padded to 1), grown by a relative 1e-9 so it contains the engine's box despite rounding
+    Box gbox;
+    {
+        Box rb;
+        for (uint64_t s = 0; s < S; ++s)
+            if (h.kind[s] != P2M_SITE_SENTINEL) rb.add(h.sites[s]);
+        for (int c = 0; c < 3; ++c) {
+            const double l = comp(rb.lo, c), u = comp(rb.hi, c);
+            const double mid = 0.5 * (l + u);
+            double hh = 0.75 * (u - l);
+            if (!(hh > 0)) hh = 1.0;
+            hh *= 1.0 + 1e-9;
+            (c == 0 ? gbox.lo.x : c == 1 ? gbox.lo.y : gbox.lo.z) = mid - hh;
+            (c == 0 ? gbox.hi.x : c == 1 ? gbox.hi.y : gbox.hi.z) = mid + hh;
+        }
+    }
     std::vector<uint64_t> ncorner(threads, 0);
     double t_cells = 0.0;
     std::vector<double> tcell(threads, 0.0);
@@ -332,8 +349,10 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
             tcell[w] += tc.s();
             ncorner[w] += corners.size();
             {
-                Box cb;
-                for (const V3& u : corners) cb.add(u);
+                // box of (cell ∩ grid box): the device's exact cell-locate grid only answers points
+                // inside the grid box, so clipping first keeps it exact and much tighter for cells
+                // that reach the sentinels (outward cones)
+                const Box cb = cc.clipped_box((uint32_t)s, gbox);
                 double* o = &h.cell_box[6 * s];
                 o[0] = cb.lo.x; o[1] = cb.lo.y; o[2] = cb.lo.z; o[3] = cb.hi.x; o[4] = cb.hi.y; o[5] = cb.hi.z;
             }

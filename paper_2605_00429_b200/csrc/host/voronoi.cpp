@@ -153,6 +153,20 @@ bool CellClipper::clip(V3 n, double d, int nb) {
     return true;
 }
 
+Box CellClipper::clipped_box(uint32_t site, const Box& b) {
+    const V3 v = S_[site];
+    const V3 lo = b.lo - v, hi = b.hi - v;
+    clip(V3{1, 0, 0}, hi.x, -11);
+    clip(V3{-1, 0, 0}, -lo.x, -12);
+    clip(V3{0, 1, 0}, hi.y, -13);
+    clip(V3{0, -1, 0}, -lo.y, -14);
+    clip(V3{0, 0, 1}, hi.z, -15);
+    clip(V3{0, 0, -1}, -lo.z, -16);
+    Box out;
+    for (const V3& p : P_) out.add(v + p);
+    return out;
+}
+
 void CellClipper::compute(uint32_t site, std::vector<V3>& corners, std::vector<uint32_t>* nbrs) {
     const V3 v = S_[site];
     init_box(v);

@@ -32,6 +32,10 @@ class CellClipper {
     // corners (absolute positions) and Delaunay neighbours (sites whose bisector bounds a face)
     void compute(uint32_t site, std::vector<V3>& corners, std::vector<uint32_t>* nbrs);
 
+    // After compute(site): clip the cell to box b (the device's cell-locate grid box) and return
+    // the bounding box of what remains -- a tight, conservative box of cell ∩ b.  Destroys the cell.
+    Box clipped_box(uint32_t site, const Box& b);
+
     uint64_t clips() const { return clips_; }
 
    private:
