@@ -52,6 +52,9 @@ def _bind(L):
     L.orc_ctx_free.argtypes = [C.c_void_p]
     L.orc_batch_query.argtypes = [C.c_void_p, dp, C.c_uint64, C.c_int, C.c_int, dp, dp, u32p, u32p, u32p,
                                   u64p, C.POINTER(Counters)]
+    L.orc_walk_nearest.restype = C.c_uint32
+    L.orc_walk_nearest.argtypes = [dp, u64p, u32p, C.c_uint64, dp, C.c_uint32, dp, u64p]
+    L.orc_batch_walk.argtypes = [dp, u64p, u32p, C.c_uint64, dp, C.c_uint64, C.c_int, u32p, u64p]
     L.orc_max_threads.restype = C.c_int
     L.orc_uses_reference_kernel.restype = C.c_int
     return L
@@ -201,6 +204,32 @@ class OracleEngine:
         if per_query:
             out["per_query"] = pq
         return out
+
+
+def walk_nearest(sites, adj_off, adj, q, start=0):
+    """DelaunayWalk nearest site (REF/SPEC.md:476): (site, d2, steps)."""
+    xyz = np.ascontiguousarray(sites, dtype=np.float64).reshape(-1, 3)
+    ao = np.ascontiguousarray(adj_off, dtype=np.uint64)
+    aj = np.ascontiguousarray(adj, dtype=np.uint32)
+    qq = np.ascontiguousarray(q, dtype=np.float64).reshape(3)
+    d2 = C.c_double()
+    st = C.c_uint64(0)
+    s = lib().orc_walk_nearest(_p(xyz), _p(ao, u64p), _p(aj, u32p), len(xyz), _p(qq), int(start),
+                               C.byref(d2), C.byref(st))
+    return int(s), d2.value, int(st.value)
+
+
+def batch_walk(sites, adj_off, adj, q, threads=0):
+    """Batch DelaunayWalk with the SPEC's per-thread warm start (REF/SPEC.md:516): (sites, steps)."""
+    xyz = np.ascontiguousarray(sites, dtype=np.float64).reshape(-1, 3)
+    ao = np.ascontiguousarray(adj_off, dtype=np.uint64)
+    aj = np.ascontiguousarray(adj, dtype=np.uint32)
+    qq = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
+    out = np.empty(len(qq), np.uint32)
+    st = C.c_uint64(0)
+    lib().orc_batch_walk(_p(xyz), _p(ao, u64p), _p(aj, u32p), len(xyz), _p(qq), len(qq), threads,
+                         _p(out, u32p), C.byref(st))
+    return out, int(st.value)
 
 
 def max_threads(reference=False) -> int:

@@ -10,6 +10,7 @@
  *     (Ericson Voronoi-region test; same operation order, no FMA -> bitwise equal d^2 / point)
  *   - minimal bounding sphere of a triangle:          REF/proj/src/geom.cpp:96-120
  *   - nearest_site (exact, ties -> lowest site id):    REF/SPEC.md:463-466, 482-487
+ *   - DelaunayWalk nearest_site (greedy + tie flood):  REF/SPEC.md:476, 516
  *   - query_distance (pruned scan, d_min=+inf, strict): REF/SPEC.md:488-496, 513-515
  *   - batch_query (per-thread counters merged):        REF/SPEC.md:497-505, 518-519
  *   - brute_force_closest (lowest face id on ties):    REF/SPEC.md:536-544
@@ -276,6 +277,87 @@ ORC_EXPORT uint32_t orc_nearest_site_brute(const double *xyz, uint64_t n, const 
     }
     if (d2_out) *d2_out = best;
     return id;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * DelaunayWalk nearest_site (REF/SPEC.md:476, 516): greedy descent on the Delaunay adjacency --
+ * move to the neighbour with the smallest (d^2, id) while it beats the current site; on a
+ * Delaunay graph the local minimum is the global nearest distance.  Equidistant sites need not be
+ * adjacent to each other along an improving path (four cospherical sites around a Voronoi edge
+ * form a cycle), so the walk then floods the tie set -- every site reachable through sites at
+ * exactly the minimum d^2 -- and returns its lowest id (ties -> lowest site id, REF/SPEC.md:465).
+ * steps (optional) counts the moves.  Restated for the strategy-neutrality check of
+ * REF/SPEC.md:510; the device walk (p2m_traverse.cuh) follows the same definition.
+ */
+ORC_EXPORT uint32_t orc_walk_nearest(const double *xyz, const uint64_t *adj_off, const uint32_t *adj,
+                                     uint64_t n_sites, const double *q, uint32_t start, double *d2_out,
+                                     uint64_t *steps) {
+    uint32_t v = start < n_sites ? start : 0;
+    double dv = dist2_3(q, xyz + 3 * (uint64_t)v);
+    uint64_t st = 0;
+    for (;;) {
+        uint32_t b = v;
+        double bd = dv;
+        for (uint64_t k = adj_off[v]; k < adj_off[v + 1]; ++k) {
+            const uint32_t w = adj[k];
+            const double d = dist2_3(q, xyz + 3 * (uint64_t)w);
+            if (d < bd || (d == bd && w < b)) { b = w; bd = d; }
+        }
+        if (b == v) break;
+        v = b; dv = bd; ++st;
+    }
+    /* tie flood */
+    uint64_t cap = 64, n = 0, head = 0;
+    uint32_t *set = (uint32_t *)malloc(cap * sizeof(uint32_t));
+    uint32_t best = v;
+    if (set) {
+        set[n++] = v;
+        while (head < n) {
+            const uint32_t u = set[head++];
+            for (uint64_t k = adj_off[u]; k < adj_off[u + 1]; ++k) {
+                const uint32_t w = adj[k];
+                if (dist2_3(q, xyz + 3 * (uint64_t)w) != dv) continue;
+                int seen = 0;
+                for (uint64_t i = 0; i < n; ++i) if (set[i] == w) { seen = 1; break; }
+                if (seen) continue;
+                if (n == cap) {
+                    uint32_t *ns = (uint32_t *)realloc(set, 2 * cap * sizeof(uint32_t));
+                    if (!ns) break;
+                    set = ns; cap *= 2;
+                }
+                set[n++] = w;
+                if (w < best) best = w;
+            }
+        }
+        free(set);
+    }
+    if (d2_out) *d2_out = dv;
+    if (steps) *steps += st;
+    return best;
+}
+
+/* Batch walk with the SPEC's warm start: each thread's first query starts at site 0 and every
+ * later query at the previous query's answer (REF/SPEC.md:516, per-thread state REF/SPEC.md:520). */
+ORC_EXPORT void orc_batch_walk(const double *xyz, const uint64_t *adj_off, const uint32_t *adj,
+                               uint64_t n_sites, const double *q, uint64_t n, int threads,
+                               uint32_t *site, uint64_t *total_steps) {
+    uint64_t ts = 0;
+#ifdef _OPENMP
+    if (threads <= 0) threads = omp_get_max_threads();
+#pragma omp parallel num_threads(threads) reduction(+ : ts)
+#endif
+    {
+        uint32_t prev = 0;
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+        for (int64_t i = 0; i < (int64_t)n; ++i) {
+            prev = orc_walk_nearest(xyz, adj_off, adj, n_sites, q + 3 * i, prev, NULL, &ts);
+            site[i] = prev;
+        }
+    }
+    (void)threads;
+    if (total_steps) *total_steps = ts;
 }
 
 /* ------------------------------------------------------------------------------------------

@@ -5,6 +5,7 @@ Build once on the host (HostEngine.build), upload (Engine), query on the GPU (En
 from .engine import (  # noqa: F401
     BatchResult,
     BuildConfig,
+    delaunay_adjacency,
     Engine,
     HostEngine,
     QueryResult,

@@ -44,6 +44,8 @@ class EngineDesc(C.Structure):
         ("domain_max", C.c_double * 3),
         ("site_cell_box", dp),
         ("site_ref_xyz", dp),
+        ("adj_offsets", u64p),
+        ("adj_sites", u32p),
     ]
 
 
@@ -104,6 +106,25 @@ class BuildStats(C.Structure):
         return {k: (getattr(self, k)) for k, _ in self._fields_}
 
 
+class TableJob(C.Structure):
+    """p2m_table_job (include/p2m.h)."""
+
+    _fields_ = [
+        ("n_sites", C.c_uint64),
+        ("ball_off", u64p),
+        ("balls", dp),
+        ("n_faces", C.c_uint64),
+        ("tri", dp),
+        ("n_nodes", C.c_uint64),
+        ("node_box", dp),
+        ("node_meta", u32p),
+        ("perm", u32p),
+    ]
+
+
+TABLE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, u64p, C.POINTER(u32p))
+
+
 class P2MError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"{ERRORS.get(code, code)}: {msg}")
@@ -131,6 +152,8 @@ def host() -> C.CDLL:
         L.p2m_last_error.restype = C.c_char_p
         L.p2m_build_config_default.argtypes = [C.POINTER(BuildConfig)]
         L.p2m_build.argtypes = [dp, C.c_uint64, u32p, C.c_uint64, C.POINTER(BuildConfig), C.POINTER(C.c_void_p)]
+        L.p2m_build_with.argtypes = [dp, C.c_uint64, u32p, C.c_uint64, C.POINTER(BuildConfig), C.c_void_p,
+                                     C.c_void_p, C.POINTER(C.c_void_p)]
         L.p2m_host_engine_destroy.argtypes = [C.c_void_p]
         L.p2m_host_engine_desc.argtypes = [C.c_void_p, C.POINTER(EngineDesc)]
         L.p2m_host_engine_stats.argtypes = [C.c_void_p, C.POINTER(BuildStats)]
@@ -145,6 +168,7 @@ def host() -> C.CDLL:
         L.p2m_gen_queries.argtypes = [C.c_int, dp, C.c_uint64, u32p, C.c_uint64, C.c_uint64, C.c_uint64, dp]
         L.p2m_gen_uniform.argtypes = [C.c_uint64, dp, dp, C.c_uint64, C.c_uint64, dp]
         L.p2m_free.argtypes = [C.c_void_p]
+        L.p2m_delaunay_adjacency.argtypes = [dp, C.c_uint64, C.POINTER(u64p), C.POINTER(u32p)]
         _host = L
     return _host
 
@@ -167,6 +191,9 @@ def cuda() -> C.CDLL:
         L.p2m_last_timings.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
         L.p2m_kernels_per_query.argtypes = [vp, C.c_uint64, C.POINTER(C.c_int)]
         L.p2m_set_scan_mode.argtypes = [vp, C.c_int]
+        L.p2m_set_nns_strategy.argtypes = [vp, C.c_int]
+        L.p2m_build_device.argtypes = [dp, C.c_uint64, u32p, C.c_uint64, C.POINTER(BuildConfig), C.c_int, C.POINTER(vp)]
+        L.p2m_table_job_device.argtypes = [vp, vp, u64p, C.POINTER(u32p)]
         _cuda = L
     return _cuda
 

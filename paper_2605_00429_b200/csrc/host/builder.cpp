@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -120,6 +121,8 @@ static void face_arrays(HostEngine& h) {
     }
 }
 
+static void build_adjacency(HostEngine& h, std::vector<std::vector<uint32_t>>& nbr);
+
 static Box outer_box(const HostEngine& h) {
     // cube about D's centre that contains every sentinel-bounded cell (<= 2x the sentinel
     // half-extent along any axis for sites inside D); 3x for margin
@@ -137,6 +140,42 @@ static constexpr int kKnn = 24;
 void cell_corners(const HostEngine& h, uint32_t site, std::vector<V3>& out) {
     CellClipper cc(h.sites, h.tree, outer_box(h), h.sentinel_ids, 8, h.eps, kKnn);
     cc.compute(site, out, nullptr);
+}
+
+void delaunay_adjacency(const double* xyz, uint64_t n, int n_threads, std::vector<uint64_t>& off,
+                        std::vector<uint32_t>& adj) {
+    // the builder's bounded site set (REF/SPEC.md:247-255) around the points, cells by clipping
+    HostEngine h;
+    Box aabb;
+    for (uint64_t i = 0; i < n; ++i) aabb.add(ld3(xyz + 3 * i));
+    h.D = aabb.scaled(10.0, 0.1);
+    h.sentinel_box = h.D.scaled(4.0, 0.0);
+    h.eps = 1e-12 * h.D.diag();
+    for (uint64_t i = 0; i < n; ++i) h.sites.push_back(ld3(xyz + 3 * i));
+    for (int i = 0; i < 8; ++i) {
+        h.sentinel_ids[i] = (uint32_t)h.sites.size();
+        h.sites.push_back(V3{(i & 1) ? h.sentinel_box.hi.x : h.sentinel_box.lo.x,
+                             (i & 2) ? h.sentinel_box.hi.y : h.sentinel_box.lo.y,
+                             (i & 4) ? h.sentinel_box.hi.z : h.sentinel_box.lo.z});
+    }
+    h.tree.build(h.sites);
+    const Box outer = outer_box(h);
+    std::vector<std::vector<uint32_t>> nbr(n + 8);
+    parallel_for(n, hw_threads(n_threads), 32, [&](uint64_t b, uint64_t e, int) {
+        CellClipper cc(h.sites, h.tree, outer, h.sentinel_ids, 8, h.eps, kKnn);
+        std::vector<V3> corners;
+        for (uint64_t s = b; s < e; ++s) cc.compute((uint32_t)s, corners, &nbr[s]);
+    });
+    build_adjacency(h, nbr);
+    // drop the sentinels: for q inside D = AABB x 10 a sentinel is never closer than the current
+    // site of a walk that starts at a real site, so the walk never needs them
+    off.assign(n + 1, 0);
+    adj.clear();
+    for (uint64_t s = 0; s < n; ++s) {
+        for (uint64_t k = h.adj_off[s]; k < h.adj_off[s + 1]; ++k)
+            if (h.adj[k] < n) adj.push_back(h.adj[k]);
+        off[s + 1] = adj.size();
+    }
 }
 
 void finish_engine(HostEngine& h) {
@@ -157,6 +196,76 @@ static void prep_mesh(const double* v, uint64_t nv, const uint32_t* f, uint64_t 
     for (uint64_t i = 0; i < h.V.size() / 3; ++i) h.aabb.add(ld3(&h.V[3 * i]));
 }
 
+// Delaunay adjacency CSR: the union of both directions of every facet-neighbour relation (a facet
+// dropped within the clipping tolerance on one side is still an edge), sorted per site.
+static void build_adjacency(HostEngine& h, std::vector<std::vector<uint32_t>>& nbr) {
+    const uint64_t S = nbr.size();
+    std::vector<uint64_t> cnt(S + 1, 0);
+    for (uint64_t s = 0; s < S; ++s)
+        for (uint32_t w : nbr[s]) { ++cnt[s + 1]; ++cnt[w + 1]; }
+    for (uint64_t s = 0; s < S; ++s) cnt[s + 1] += cnt[s];
+    std::vector<uint32_t> all(cnt[S]);
+    std::vector<uint64_t> cur(cnt.begin(), cnt.end() - 1);
+    for (uint64_t s = 0; s < S; ++s)
+        for (uint32_t w : nbr[s]) { all[cur[s]++] = w; all[cur[w]++] = (uint32_t)s; }
+    h.adj_off.assign(S + 1, 0);
+    h.adj.clear();
+    h.adj.reserve(all.size() / 2 + 16);
+    for (uint64_t s = 0; s < S; ++s) {
+        auto b = all.begin() + cnt[s], e = all.begin() + cnt[s + 1];
+        std::sort(b, e);
+        e = std::unique(b, e);
+        for (auto it = b; it != e; ++it)
+            if (*it != s) h.adj.push_back(*it);
+        h.adj_off[s + 1] = h.adj.size();
+        std::vector<uint32_t>().swap(nbr[s]);
+    }
+}
+
+// Flatten the per-site balls and the BVH into a p2m_table_job and run the delegated executor.
+static void run_table_job(HostEngine& h, std::vector<std::vector<Ball>>& site_balls, p2m_table_fn fn,
+                          void* ctx) {
+    const uint64_t S = site_balls.size();
+    std::vector<uint64_t> boff(S + 1, 0);
+    for (uint64_t s = 0; s < S; ++s) boff[s + 1] = boff[s] + site_balls[s].size();
+    std::vector<double> balls(4 * boff[S]);
+    for (uint64_t s = 0; s < S; ++s) {
+        double* o = &balls[4 * boff[s]];
+        for (const Ball& b : site_balls[s]) { o[0] = b.c.x; o[1] = b.c.y; o[2] = b.c.z; o[3] = b.r2; o += 4; }
+        std::vector<Ball>().swap(site_balls[s]);
+    }
+    const auto& nodes = h.bvh.nodes();
+    std::vector<double> nbox(6 * nodes.size());
+    std::vector<uint32_t> nmeta(3 * nodes.size());
+    for (size_t i = 0; i < nodes.size(); ++i) {
+        const BvhNode& n = nodes[i];
+        double* b = &nbox[6 * i];
+        b[0] = n.box.lo.x; b[1] = n.box.lo.y; b[2] = n.box.lo.z; b[3] = n.box.hi.x; b[4] = n.box.hi.y; b[5] = n.box.hi.z;
+        nmeta[3 * i] = n.right; nmeta[3 * i + 1] = n.first; nmeta[3 * i + 2] = n.count;
+    }
+    p2m_table_job job{};
+    job.n_sites = S;
+    job.ball_off = boff.data();
+    job.balls = balls.data();
+    job.n_faces = h.tri.size() / 9;
+    job.tri = h.tri.data();
+    job.n_nodes = nodes.size();
+    job.node_box = nbox.data();
+    job.node_meta = nmeta.data();
+    job.perm = h.bvh.perm().data();
+    uint32_t* lists = nullptr;
+    const int rc = fn(ctx, &job, h.off.data(), &lists);
+    if (rc != 0) {
+        std::free(lists);
+        throw std::runtime_error(std::string("build_all_tables: table executor failed (") + std::to_string(rc) + "): " + get_error());
+    }
+    if (h.off[0] != 0) { std::free(lists); throw std::runtime_error("build_all_tables: bad offsets from executor"); }
+    for (uint64_t s = 0; s < S; ++s)
+        if (h.off[s + 1] < h.off[s]) { std::free(lists); throw std::runtime_error("build_all_tables: bad offsets from executor"); }
+    h.lists.assign(lists, lists + h.off[S]);
+    std::free(lists);
+}
+
 std::unique_ptr<HostEngine> build_engine_mesh_only(const double* v, uint64_t nv, const uint32_t* f,
                                                    uint64_t nf, const p2m_build_config& cfg) {
     auto hp = std::make_unique<HostEngine>();
@@ -166,7 +275,8 @@ std::unique_ptr<HostEngine> build_engine_mesh_only(const double* v, uint64_t nv,
 }
 
 std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uint32_t* f, uint64_t nf,
-                                         const p2m_build_config& cfg) {
+                                         const p2m_build_config& cfg, p2m_table_fn table_fn,
+                                         void* table_ctx) {
     Timer total;
     auto hp = std::make_unique<HostEngine>();
     HostEngine& h = *hp;
@@ -315,6 +425,8 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
     Timer tt;
     const uint64_t S = h.sites.size();
     std::vector<std::vector<uint32_t>> per(S);
+    std::vector<std::vector<Ball>> site_balls(table_fn ? S : 0);  // delegated table job
+    std::vector<std::vector<uint32_t>> nbr(S);                    // facet neighbours per cell
     h.cell_box.assign(6 * S, std::nan(""));
     // the device's grid box (p2m_engine.cu: 1.5x the real sites' AABB about its centre, a flat axis
     // padded to 1), grown by a relative 1e-9 so it contains the engine's box despite rounding
@@ -345,7 +457,7 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
         for (uint64_t s = b; s < e; ++s) {
             if (h.kind[s] == P2M_SITE_SENTINEL) continue;  // empty list (REF/SPEC.md:418)
             Timer tc;
-            cc.compute((uint32_t)s, corners, nullptr);
+            cc.compute((uint32_t)s, corners, &nbr[s]);
             tcell[w] += tc.s();
             ncorner[w] += corners.size();
             {
@@ -376,21 +488,32 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
                 for (const V3& u : corners) r = std::max(r, std::sqrt(d2(site, u)) + std::sqrt(d2(u, pr)));
                 balls.push_back(Ball{site, inflate(r)});
             }
+            if (table_fn) { site_balls[s] = balls; continue; }
             h.bvh.balls_query(balls.data(), (int)balls.size(), per[s], mark);
             std::sort(per[s].begin(), per[s].end());
         }
     });
     for (double x : tcell) t_cells += x;
+    double t_job = 0.0;
     h.off.assign(S + 1, 0);
-    for (uint64_t s = 0; s < S; ++s) h.off[s + 1] = h.off[s] + per[s].size();
-    h.lists.resize(h.off[S]);
+    if (table_fn) {
+        Timer tj;
+        run_table_job(h, site_balls, table_fn, table_ctx);
+        t_job = tj.s();
+    } else {
+        for (uint64_t s = 0; s < S; ++s) h.off[s + 1] = h.off[s] + per[s].size();
+        h.lists.resize(h.off[S]);
+        for (uint64_t s = 0; s < S; ++s) {
+            std::copy(per[s].begin(), per[s].end(), h.lists.begin() + h.off[s]);
+            std::vector<uint32_t>().swap(per[s]);
+        }
+    }
     uint64_t lmax = 0, real = 0;
     for (uint64_t s = 0; s < S; ++s) {
-        std::copy(per[s].begin(), per[s].end(), h.lists.begin() + h.off[s]);
-        lmax = std::max<uint64_t>(lmax, per[s].size());
+        lmax = std::max<uint64_t>(lmax, h.off[s + 1] - h.off[s]);
         if (h.kind[s] != P2M_SITE_SENTINEL) ++real;
-        std::vector<uint32_t>().swap(per[s]);
     }
+    build_adjacency(h, nbr);
     h.stats.list_entries = h.off[S];
     h.stats.list_max = lmax;
     h.stats.list_avg = real ? (double)h.off[S] / (double)real : 0.0;
@@ -401,11 +524,11 @@ std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uin
     h.stats.n_aux_sites = S - NV - 8;
     // Table-3 split: "voronoi" = the cell passes of the augmentation rounds plus the final cell
     // construction (thread-summed time rescaled to the final pass's wall time), "tables" = rest
-    const double wall = tt.s();
+    const double wall = tt.s() - t_job;
     double cell_cpu = t_cells, all_cpu = wall * threads;
     const double cell_wall = all_cpu > 0 ? wall * std::min(1.0, cell_cpu / all_cpu) : 0.0;
     h.stats.t_voronoi_s = t_vor + cell_wall;
-    h.stats.t_tables_s = wall - cell_wall;
+    h.stats.t_tables_s = wall - cell_wall + t_job;
     finish_engine(h);
     h.stats.t_total_s = total.s();
     // sentinel guarantee (REF/SPEC.md:250, 287): no sentinel is nearest inside D

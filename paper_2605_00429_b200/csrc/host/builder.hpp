@@ -40,6 +40,9 @@ struct HostEngine {
     // interception index (REF/SPEC.md:391-394) as CSR
     std::vector<uint64_t> off;
     std::vector<uint32_t> lists;
+    // Delaunay adjacency (facet neighbours of the final cells, symmetrised) as CSR
+    std::vector<uint64_t> adj_off;
+    std::vector<uint32_t> adj;
     uint64_t mesh_hash = 0;
     // final site tree, kept to recompute cell corners on demand
     SiteTree tree;
@@ -47,13 +50,19 @@ struct HostEngine {
 };
 
 // Throws std::invalid_argument / std::runtime_error with a message; the C ABI maps them.
+// table_fn != nullptr: the table phase is delegated (p2m_build_with, include/p2m.h)
 std::unique_ptr<HostEngine> build_engine(const double* v, uint64_t nv, const uint32_t* f,
-                                         uint64_t nf, const p2m_build_config& cfg);
+                                         uint64_t nf, const p2m_build_config& cfg,
+                                         p2m_table_fn table_fn = nullptr, void* table_ctx = nullptr);
 std::unique_ptr<HostEngine> build_engine_mesh_only(const double* v, uint64_t nv, const uint32_t* f,
                                                    uint64_t nf, const p2m_build_config& cfg);
 void cell_corners(const HostEngine& h, uint32_t site, std::vector<V3>& out);
 uint64_t hash_mesh(const double* v, uint64_t nv, const uint32_t* f, uint64_t nf);
 void finish_engine(HostEngine& h);  // derived arrays after load
+// Delaunay adjacency of an arbitrary point set (facet neighbours of its sentinel-bounded Voronoi
+// cells, symmetric, sentinels dropped): the graph of the DelaunayWalk strategy (REF/SPEC.md:476)
+void delaunay_adjacency(const double* xyz, uint64_t n, int n_threads, std::vector<uint64_t>& off,
+                        std::vector<uint32_t>& adj);
 
 
 }  // namespace p2m

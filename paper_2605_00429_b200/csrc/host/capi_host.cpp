@@ -18,6 +18,7 @@
 namespace p2m {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+std::string get_error() { return g_err; }
 }  // namespace p2m
 
 struct p2m_host_engine {
@@ -76,6 +77,19 @@ P2M_API int p2m_build(const double* vertices, uint64_t n_vertices, const uint32_
     });
 }
 
+P2M_API int p2m_build_with(const double* vertices, uint64_t n_vertices, const uint32_t* faces,
+                           uint64_t n_faces, const p2m_build_config* cfg, p2m_table_fn fn, void* ctx,
+                           p2m_host_engine** out) {
+    return guarded([&] {
+        if (!vertices || !faces || !out) throw std::invalid_argument("p2m_build_with: null pointer");
+        p2m_build_config c;
+        if (cfg) c = *cfg; else p2m_build_config_default(&c);
+        auto h = p2m::build_engine(vertices, n_vertices, faces, n_faces, c, fn, ctx);
+        *out = new p2m_host_engine{std::move(h)};
+        return (int)P2M_OK;
+    });
+}
+
 P2M_API void p2m_host_engine_destroy(p2m_host_engine* h) { delete h; }
 
 P2M_API int p2m_host_engine_desc(const p2m_host_engine* he, p2m_engine_desc* d) {
@@ -92,6 +106,8 @@ P2M_API int p2m_host_engine_desc(const p2m_host_engine* he, p2m_engine_desc* d) 
         d->list_faces = h.lists.data();
         d->site_cell_box = h.cell_box.empty() ? nullptr : h.cell_box.data();
         d->site_ref_xyz = h.refs.empty() ? nullptr : h.refs.data();
+        d->adj_offsets = h.adj_off.empty() ? nullptr : h.adj_off.data();
+        d->adj_sites = h.adj_off.empty() ? nullptr : h.adj.data();
         d->domain_min[0] = h.D.lo.x; d->domain_min[1] = h.D.lo.y; d->domain_min[2] = h.D.lo.z;
         d->domain_max[0] = h.D.hi.x; d->domain_max[1] = h.D.hi.y; d->domain_max[2] = h.D.hi.z;
         return (int)P2M_OK;
@@ -153,7 +169,7 @@ P2M_API int p2m_host_closest_point(const p2m_host_engine* he, const double* q, d
 // EngineIndexFile (REF/SPEC.md:588-591): magic "P2MX", LE u32 version, mesh hash, D, sites
 // (kind, position, reference), per-site table offsets + face ids, config echo.  The BVH and the
 // NNS index are rebuilt on load (REF/SPEC.md:639).
-static const uint32_t kFileVersion = 2;  // v2 adds the Voronoi cell boxes
+static const uint32_t kFileVersion = 3;  // v2 adds the Voronoi cell boxes, v3 the Delaunay adjacency
 
 P2M_API int p2m_host_engine_save(const p2m_host_engine* he, const char* path) {
     return guarded([&] {
@@ -179,6 +195,10 @@ P2M_API int p2m_host_engine_save(const p2m_host_engine* he, const char* path) {
         w(h.off.data(), 8 * (S + 1));
         w(h.lists.data(), 4 * h.lists.size());
         w(h.cell_box.data(), 8 * h.cell_box.size());
+        const uint64_t na = h.adj.size();
+        w(&na, 8);
+        w(h.adj_off.data(), 8 * h.adj_off.size());
+        w(h.adj.data(), 4 * na);
         w("XM2P", 4);
         ok = (std::fclose(fp) == 0) && ok;
         if (!ok) { set_error("write failed"); return (int)P2M_ERR_IO; }
@@ -240,6 +260,14 @@ P2M_API int p2m_host_engine_load(const char* path, const double* vertices, uint6
         r(h.lists.data(), 4 * h.lists.size());
         h.cell_box.resize(6 * S);
         r(h.cell_box.data(), 8 * h.cell_box.size());
+        uint64_t na = 0;
+        r(&na, 8);
+        if (!ok || na > (1ull << 36)) { std::fclose(fp); set_error("EngineIndexFile truncated (adjacency)"); return (int)P2M_ERR_IO; }
+        h.adj_off.resize(S + 1);
+        h.adj.resize(na);
+        r(h.adj_off.data(), 8 * (S + 1));
+        r(h.adj.data(), 4 * na);
+        if (ok && (h.adj_off[0] != 0 || h.adj_off[S] != na)) { std::fclose(fp); set_error("EngineIndexFile corrupt (adjacency)"); return (int)P2M_ERR_IO; }
         char tail[4] = {0};
         r(tail, 4);
         std::fclose(fp);
@@ -249,6 +277,21 @@ P2M_API int p2m_host_engine_load(const char* path, const double* vertices, uint6
         h.bvh.build(h.tri.data(), h.F.size() / 3, 4);
         p2m::finish_engine(h);
         *out = new p2m_host_engine{std::move(hp)};
+        return (int)P2M_OK;
+    });
+}
+
+P2M_API int p2m_delaunay_adjacency(const double* xyz, uint64_t n, uint64_t** off, uint32_t** adj) {
+    return guarded([&] {
+        if (!xyz || !off || !adj || n == 0) throw std::invalid_argument("p2m_delaunay_adjacency: bad argument");
+        std::vector<uint64_t> o;
+        std::vector<uint32_t> a;
+        p2m::delaunay_adjacency(xyz, n, 0, o, a);
+        *off = (uint64_t*)std::malloc(8 * o.size());
+        *adj = (uint32_t*)std::malloc(4 * std::max<size_t>(1, a.size()));
+        if (!*off || !*adj) { std::free(*off); std::free(*adj); *off = nullptr; *adj = nullptr; throw std::bad_alloc(); }
+        std::memcpy(*off, o.data(), 8 * o.size());
+        if (!a.empty()) std::memcpy(*adj, a.data(), 4 * a.size());
         return (int)P2M_OK;
     });
 }

@@ -68,5 +68,6 @@ struct Timer {
 };
 
 void set_error(const std::string& msg);
+std::string get_error();
 
 }  // namespace p2m

@@ -77,11 +77,65 @@ class HostEngine:
         self._keep = keep
 
     @classmethod
-    def build(cls, vertices, faces, config: Optional[BuildConfig] = None) -> "HostEngine":
+    def build(cls, vertices, faces, config: Optional[BuildConfig] = None,
+              table_device: Optional[int] = None) -> "HostEngine":
+        """cmd_build (REF/SPEC.md:598-606).  table_device=k runs build_all_tables on GPU k
+        (p2m_build_device, bit-identical tables); None keeps the whole build on host threads."""
         v, f = _as_mesh(vertices, faces)
         cfg = (config or BuildConfig()).to_c()
         h = C.c_void_p()
-        L.check(L.host().p2m_build(L.ptr(v), len(v), L.ptr(f, L.u32p), len(f), C.byref(cfg), C.byref(h)))
+        if table_device is None:
+            L.check(L.host().p2m_build(L.ptr(v), len(v), L.ptr(f, L.u32p), len(f), C.byref(cfg), C.byref(h)))
+        else:
+            L.check(L.cuda().p2m_build_device(L.ptr(v), len(v), L.ptr(f, L.u32p), len(f), C.byref(cfg),
+                                              int(table_device), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def build_with(cls, vertices, faces, table_fn, config: Optional[BuildConfig] = None) -> "HostEngine":
+        """p2m_build_with: table_fn(job) -> (off[S+1] uint64, lists uint32) runs the table job
+        (include/p2m.h p2m_table_job, exposed as numpy arrays)."""
+        v, f = _as_mesh(vertices, faces)
+        cfg = (config or BuildConfig()).to_c()
+        h = C.c_void_p()
+        libc = C.CDLL(None)
+        libc.malloc.restype = C.c_void_p
+        libc.malloc.argtypes = [C.c_size_t]
+        err = []
+
+        def _cb(ctx, job_p, off_p, lists_pp):
+            try:
+                j = C.cast(job_p, C.POINTER(L.TableJob)).contents
+                S, NF, NN = j.n_sites, j.n_faces, j.n_nodes
+                boff = np.ctypeslib.as_array(j.ball_off, (S + 1,)).copy()
+                nb = int(boff[-1])
+                job = {
+                    "ball_off": boff,
+                    "balls": np.ctypeslib.as_array(j.balls, (max(nb, 1) * 4,))[: 4 * nb].reshape(-1, 4).copy(),
+                    "tri": np.ctypeslib.as_array(j.tri, (max(NF, 1) * 9,))[: 9 * NF].reshape(-1, 9).copy(),
+                    "node_box": np.ctypeslib.as_array(j.node_box, (max(NN, 1) * 6,))[: 6 * NN].reshape(-1, 6).copy(),
+                    "node_meta": np.ctypeslib.as_array(j.node_meta, (max(NN, 1) * 3,))[: 3 * NN].reshape(-1, 3).copy(),
+                    "perm": np.ctypeslib.as_array(j.perm, (max(NF, 1),))[:NF].copy(),
+                }
+                off, lists = table_fn(job)
+                off = np.ascontiguousarray(off, dtype=np.uint64)
+                lists = np.ascontiguousarray(lists, dtype=np.uint32)
+                C.memmove(off_p, off.ctypes.data, 8 * (S + 1))
+                buf = libc.malloc(max(4 * len(lists), 4))
+                if len(lists):
+                    C.memmove(buf, lists.ctypes.data, 4 * len(lists))
+                lists_pp[0] = C.cast(buf, L.u32p)
+                return 0
+            except Exception as e:  # surfaced through p2m_last_error
+                err.append(e)
+                return -7
+
+        cb = L.TABLE_FN(_cb)
+        rc = L.host().p2m_build_with(L.ptr(v), len(v), L.ptr(f, L.u32p), len(f), C.byref(cfg),
+                                      C.cast(cb, C.c_void_p), None, C.byref(h))
+        if err:
+            raise err[0]
+        L.check(rc)
         return cls(h)
 
     @classmethod
@@ -129,6 +183,11 @@ class HostEngine:
             "list_faces": np.ctypeslib.as_array(d.list_faces, shape=(L_,)) if L_ else np.zeros(0, np.uint32),
             "domain": np.array(list(d.domain_min) + list(d.domain_max)),
         }
+        if d.adj_offsets:
+            ao = np.ctypeslib.as_array(d.adj_offsets, shape=(S + 1,))
+            out["adj_offsets"] = ao
+            out["adj_sites"] = (np.ctypeslib.as_array(d.adj_sites, shape=(int(ao[-1]),)) if int(ao[-1])
+                                else np.zeros(0, np.uint32))
         refs = L.dp()
         L.check(L.host().p2m_host_engine_site_refs(self._h, C.byref(refs)))
         out["site_refs"] = np.ctypeslib.as_array(refs, shape=(S, 3))
@@ -228,6 +287,13 @@ class Engine:
     def nearest_site(self, points) -> np.ndarray:
         return self.batch_query(points).site
 
+    NNS = {"grid": 0, "kdtree": 1, "walk": 2}
+
+    def set_nns_strategy(self, strategy: str) -> None:
+        """NearestSiteIndex strategy (REF/SPEC.md:473-481): 'grid' (default), 'kdtree' or 'walk'
+        (DelaunayWalk).  Results never depend on it (strategy neutrality, REF/SPEC.md:510)."""
+        L.check(L.cuda().p2m_set_nns_strategy(self.handle, self.NNS[strategy]))
+
 
 # ---- synthetic workloads -------------------------------------------------------------------
 
@@ -258,6 +324,21 @@ def gen_queries(cfg: int, vertices, faces, first: int, count: int, out: Optional
         out = np.empty((count, 3))
     L.check(L.host().p2m_gen_queries(cfg, L.ptr(v), len(v), L.ptr(f, L.u32p), len(f), first, count, L.ptr(out)))
     return out
+
+
+def delaunay_adjacency(points):
+    """Delaunay adjacency (CSR offsets, neighbours) of an arbitrary point set -- the DelaunayWalk
+    graph (REF/SPEC.md:476), valid for queries inside 10x the points' AABB."""
+    xyz = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    o = L.u64p(); a = L.u32p()
+    L.check(L.host().p2m_delaunay_adjacency(L.ptr(xyz), len(xyz), C.byref(o), C.byref(a)))
+    try:
+        off = np.ctypeslib.as_array(o, shape=(len(xyz) + 1,)).copy()
+        adj = np.ctypeslib.as_array(a, shape=(max(1, int(off[-1])),))[: int(off[-1])].copy()
+    finally:
+        L.host().p2m_free(C.cast(o, C.c_void_p))
+        L.host().p2m_free(C.cast(a, C.c_void_p))
+    return off, adj
 
 
 def gen_uniform(seed: int, lo, hi, first: int, count: int):

@@ -215,7 +215,8 @@ def test_save_load_round_trip(ico3):
             assert f.read(4) == b"P2MX"
         h2 = P.HostEngine.load(path, V, F)
         a, b = h.arrays(), h2.arrays()
-        for k in ("site_xyz", "site_kind", "list_offsets", "list_faces", "sphere", "tri", "domain"):
+        for k in ("site_xyz", "site_kind", "list_offsets", "list_faces", "sphere", "tri", "domain",
+                  "adj_offsets", "adj_sites"):
             assert a[k].tobytes() == b[k].tobytes(), k
         q = np.random.default_rng(0).uniform(-1.2, 1.2, size=(500, 3))
         r1 = O.OracleEngine(a).batch_query(q)
