@@ -1,7 +1,7 @@
 # Top-level build: every native artefact, in-tree (the .so files travel to the GPU box with the
 # repo snapshot).  `python -c "import __graft_entry__ as g; g.build()"` runs `make -j`.
 PKG      := paper_2605_00429_b200
-LIBDIR   := $(PKG)/lib
+LIBDIR   ?= $(PKG)/lib
 HOSTSRC  := $(wildcard $(PKG)/csrc/host/*.cpp)
 HOSTHDR  := $(wildcard $(PKG)/csrc/host/*.hpp) include/p2m.h
 CUDASRC  := $(wildcard $(PKG)/csrc/cuda/*.cu)
@@ -11,7 +11,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 # fp64 parity: no contraction anywhere on the distance path
 CXXFLAGS := -O2 -g -std=gnu++17 -fPIC -ffp-contract=off -fvisibility=hidden -pthread -Wall -Wno-unused-function
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off,-fvisibility=hidden \
-            -Xptxas -v --expt-relaxed-constexpr
+            -Xptxas -v --expt-relaxed-constexpr $(NVEXTRA)
 
 all: $(LIBDIR)/libp2m_host.so $(LIBDIR)/libp2m_cuda.so oracle examples/query_demo
 

@@ -10,6 +10,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIBDIR = os.path.join(_HERE, "lib")
+LIBDIR = os.environ.get("P2M_LIB_DIR", LIBDIR)  # A/B builds of the same sources (scripts/)
 
 P2M_OK = 0
 ERRORS = {

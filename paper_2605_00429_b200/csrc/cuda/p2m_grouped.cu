@@ -197,8 +197,11 @@ constexpr int kWinChunks = 256;                  // level-0 need bits are comput
 static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 constexpr int kWarps = kTile / 32;
 
+#ifndef P2M_SCAN_MINB
+#define P2M_SCAN_MINB 3  // resident CTAs per SM the register budget is sized for
+#endif
 template <bool kCounters>
-__global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
+__global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
                                                          const uint32_t* __restrict__ rows,
                                                          const uint32_t* __restrict__ key,
                                                          const uint32_t* __restrict__ tiles,
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     __shared__ uint32_t s_oidx[kWinChunks];      // ... in visiting order
     __shared__ uint32_t s_okey[kWinChunks];
     __shared__ float4 s_qrep;                    // the tile's first row (fp32), for the visiting order
+    __shared__ uint32_t s_next;                  // small tiles: next batch of the window to scan
     __shared__ double s_rd[kTile];
     __shared__ uint32_t s_rf[kTile];
     __shared__ uint32_t s_re[kTile];
@@ -376,6 +380,132 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                 __syncthreads();
             }
         }
+        // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)},
+        // lb: 32 x 64-byte lower-bound records, fid: 32 face ids).  Each lane computes a pass/prune bit
+        // per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the warp
+        // walks the union of set bits in list order; a lane whose bit is set re-tests with its
+        // CURRENT d_min, applies the tight fp32 lower bound, and survivors run the exact fp64 kernel
+        // on the face record (all lanes read the same record: broadcast).  stage_lb: the lower-bound
+        // records of the union are loaded here (lane k holds entry k's face id my_f).
+        auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
+                              uint32_t my_f) {
+            uint32_t mask = 0;
+            if (active) {
+#pragma unroll
+                for (int pp = 0; pp < 16; ++pp) {
+                    const float4 A = pair[2 * pp], B = pair[2 * pp + 1];
+                    const uint64_t dx = sub2(QX, pk2(A.x, A.y));
+                    const uint64_t dy = sub2(QY, pk2(A.z, A.w));
+                    const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
+                    const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+                    const uint64_t th = add2_up(pk2(B.z, B.w), DK);
+                    const uint64_t t2 = mul2_up(th, th);
+                    float d0, d1, t0, t1;
+                    upk2(d2, d0, d1);
+                    upk2(t2, t0, t1);
+                    mask |= (uint32_t)(!(d0 > t0)) << (2 * pp);
+                    mask |= (uint32_t)(!(d1 > t1)) << (2 * pp + 1);
+                }
+                if (valid < 32) mask &= (1u << valid) - 1u;
+            }
+            uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+            if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
+            if (stage_lb && um) {
+                if ((um >> lane) & 1u) {
+                    const float4* lr = p.lbr + 4 * (uint64_t)my_f;
+                    lb[4 * lane] = lr[0];
+                    lb[4 * lane + 1] = lr[1];
+                    lb[4 * lane + 2] = lr[2];
+                    lb[4 * lane + 3] = lr[3];
+                }
+                __syncwarp();
+            }
+            const float* pf = reinterpret_cast<const float*>(pair);
+            while (um) {
+                const int kk = __ffs(um) - 1;
+                um &= um - 1;
+                if ((mask >> kk) & 1u) {
+                    // the batch mask used the d_min of the batch start: re-test this candidate with
+                    // the current one (same conservative fp32 sphere test, operands already in smem)
+                    {
+                        const int pp = kk >> 1, h = kk & 1;
+                        float dkx, dky;
+                        upk2(DK, dkx, dky);
+                        const float dx = qxf - pf[8 * pp + h];
+                        const float dy = qyf - pf[8 * pp + 2 + h];
+                        const float dz = qzf - pf[8 * pp + 4 + h];
+                        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                        const float th = __fadd_ru(pf[8 * pp + 6 + h], dkx);
+                        if (d2f > __fmul_ru(th, th)) continue;
+                        // then the tight lower bound
+                        const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
+                        if (lb2_face(lb + 4 * kk, qxf, qyf, qzf) > __fmul_ru(thl, thl)) continue;
+                    }
+                    const uint32_t f = fid[kk];
+                    V a, bb3, c3, pp3;
+                    load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
+                    const double dd = closest_tri(q, a, bb3, c3, &pp3);
+                    ++exact;
+                    if (dd < best || (dd == best && f < bf)) {
+                        best = dd;
+                        bf = f;
+                        dmin = sqrt(dd);
+                        const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+                        DK = pk2(dkf, dkf);
+                    }
+                }
+            }
+        };
+        if (G == 1) {
+            // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
+            // Warps pull batches of the ordered chunks from a shared counter and stage them in their
+            // own shared-memory slice -- no block barrier until the window ends, and the load
+            // balances itself (replica warps otherwise wait at every chunk for the slowest one).
+            if (tid == 0) s_next = 0u;
+            __syncthreads();
+            const uint32_t T = (uint32_t)nord * (kChunk / 32);
+            float4* wp = s_pair + 32 * w;
+            float* wpf = reinterpret_cast<float*>(wp);
+            uint32_t* wf = s_fid + 32 * w;
+            float4* wl = s_lb + 128 * w;
+            for (;;) {
+                uint32_t t = 0;
+                if (lane == 0) t = atomicAdd(&s_next, 1u);
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= T) break;
+                const uint32_t cidx = w0 + s_oidx[t / (kChunk / 32)];
+                const uint32_t gb = cidx * (kChunk / 32) + t % (kChunk / 32);  // batch index in the list
+                const uint64_t b0 = beg + 32ull * gb;
+                if (b0 >= end) continue;
+                const int valid = (int)min((uint64_t)32, end - b0);
+                bool need = p.no_batch != 0;
+                if (active && !need) {
+                    const float4 c = p.bsph[bo + gb];
+                    float dkx, dky;
+                    upk2(DK, dkx, dky);
+                    const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                    const float th = __fadd_ru(c.w, dkx);
+                    need = !(d2f > __fmul_ru(th, th));
+                }
+                if (!__any_sync(0xffffffffu, need)) continue;  // pruned whole by its batch sphere
+                uint32_t f = 0;
+                float4 rv = make_float4(finf, 0.f, 0.f, 0.f);
+                if (lane < valid) { f = p.lfs[b0 + lane]; rv = p.f32[f]; }
+                wf[lane] = f;
+                {
+                    const int pp = lane >> 1, h = lane & 1;
+                    wpf[8 * pp + h] = rv.x;
+                    wpf[8 * pp + 2 + h] = rv.y;
+                    wpf[8 * pp + 4 + h] = rv.z;
+                    wpf[8 * pp + 6 + h] = rv.w;
+                }
+                __syncwarp();
+                scan_batch(wp, wl, wf, valid, true, f);
+                __syncwarp();                    // the slice is rewritten by the next batch
+            }
+            continue;                            // next window (its first barrier orders s_next)
+        }
         for (int oi = 0; oi < nord; ++oi) {
             const uint32_t cidx = w0 + s_oidx[oi];
             const uint64_t base = beg + (uint64_t)cidx * kChunk;
@@ -451,62 +581,7 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
             for (int bb = r; bb < nb; bb += R) {
                 if (!((wneed >> bb) & 1u)) continue;  // pruned whole by its batch sphere
                 const int k0 = bb * 32;
-                uint32_t mask = 0;
-                if (active) {
-#pragma unroll
-                    for (int pp = 0; pp < 16; ++pp) {
-                        const float4 A = s_pair[k0 + 2 * pp], B = s_pair[k0 + 2 * pp + 1];
-                        const uint64_t dx = sub2(QX, pk2(A.x, A.y));
-                        const uint64_t dy = sub2(QY, pk2(A.z, A.w));
-                        const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
-                        const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-                        const uint64_t th = add2_up(pk2(B.z, B.w), DK);
-                        const uint64_t t2 = mul2_up(th, th);
-                        float d0, d1, t0, t1;
-                        upk2(d2, d0, d1);
-                        upk2(t2, t0, t1);
-                        mask |= (uint32_t)(!(d0 > t0)) << (2 * pp);
-                        mask |= (uint32_t)(!(d1 > t1)) << (2 * pp + 1);
-                    }
-                    const int valid = mc - k0;
-                    if (valid < 32) mask &= (1u << valid) - 1u;
-                }
-                uint32_t um = __reduce_or_sync(0xffffffffu, mask);
-                if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
-                while (um) {
-                    const int kk = __ffs(um) - 1;
-                    um &= um - 1;
-                    if ((mask >> kk) & 1u) {
-                        // the batch mask used the d_min of the batch start: re-test this candidate with
-                        // the current one (same conservative fp32 sphere test, operands already in smem)
-                        {
-                            const int k = k0 + kk, pp = k >> 1, h = k & 1;
-                            float dkx, dky;
-                            upk2(DK, dkx, dky);
-                            const float dx = qxf - s_pf[8 * pp + h];
-                            const float dy = qyf - s_pf[8 * pp + 2 + h];
-                            const float dz = qzf - s_pf[8 * pp + 4 + h];
-                            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                            const float th = __fadd_ru(s_pf[8 * pp + 6 + h], dkx);
-                            if (d2f > __fmul_ru(th, th)) continue;
-                            // then the tight lower bound
-                            const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-                            if (lb2_face(s_lb + 4 * k, qxf, qyf, qzf) > __fmul_ru(thl, thl)) continue;
-                        }
-                        const uint32_t f = s_fid[k0 + kk];
-                        V a, bb3, c3, pp3;
-                        load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
-                        const double dd = closest_tri(q, a, bb3, c3, &pp3);
-                        ++exact;
-                        if (dd < best || (dd == best && f < bf)) {
-                            best = dd;
-                            bf = f;
-                            dmin = sqrt(dd);
-                            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
-                            DK = pk2(dkf, dkf);
-                        }
-                    }
-                }
+                scan_batch(s_pair + k0, s_lb + 4 * k0, s_fid + k0, mc - k0, false, 0u);
             }
         }
     }

@@ -200,6 +200,12 @@ static void prep_mesh(const double* v, uint64_t nv, const uint32_t* f, uint64_t 
 // dropped within the clipping tolerance on one side is still an edge), sorted per site.
 static void build_adjacency(HostEngine& h, std::vector<std::vector<uint32_t>>& nbr) {
     const uint64_t S = nbr.size();
+    // sentinel cells are never built: their mutual facets are added as a complete graph on the 8
+    // sentinels (a supergraph of the Delaunay graph keeps the walk exact), their facets with real
+    // sites come from the real sites' cells
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j)
+            if (i != j && h.sentinel_ids[i] < S && h.sentinel_ids[j] < S) nbr[h.sentinel_ids[i]].push_back(h.sentinel_ids[j]);
     std::vector<uint64_t> cnt(S + 1, 0);
     for (uint64_t s = 0; s < S; ++s)
         for (uint32_t w : nbr[s]) { ++cnt[s + 1]; ++cnt[w + 1]; }

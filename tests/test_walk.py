@@ -64,8 +64,9 @@ def test_engine_adjacency_and_walk(ico3):
     _check_adjacency(a["adj_offsets"], a["adj_sites"], S)
     rng = np.random.default_rng(3)
     lo, hi = a["domain"][:3], a["domain"][3:]
+    # inside the mesh box, anywhere in D, at the sites, and far outside D (walks among sentinels)
     qs = np.concatenate([rng.uniform(-1.3, 1.3, (4000, 3)), rng.uniform(lo, hi, (1000, 3)),
-                         V[:200]])
+                         V[:200], rng.uniform(-40, 40, (2000, 3)), rng.uniform(-400, 400, (500, 3))])
     walk, _ = O.batch_walk(a["site_xyz"], a["adj_offsets"], a["adj_sites"], qs)
     kd = O.KdTree(a["site_xyz"])
     want = np.array([kd.nearest(q)[0] for q in qs])
