@@ -4,8 +4,9 @@ PKG      := paper_2605_00429_b200
 LIBDIR   ?= $(PKG)/lib
 HOSTSRC  := $(wildcard $(PKG)/csrc/host/*.cpp)
 HOSTHDR  := $(wildcard $(PKG)/csrc/host/*.hpp) include/p2m.h
-CUDASRC  := $(wildcard $(PKG)/csrc/cuda/*.cu)
-CUDAHDR  := $(wildcard $(PKG)/csrc/cuda/*.cuh) include/p2m.h
+CUDADIR  ?= $(PKG)/csrc/cuda
+CUDASRC  := $(wildcard $(CUDADIR)/*.cu)
+CUDAHDR  := $(wildcard $(CUDADIR)/*.cuh) include/p2m.h
 NVCC     ?= /usr/local/cuda/bin/nvcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 # fp64 parity: no contraction anywhere on the distance path

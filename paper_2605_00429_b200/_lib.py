@@ -192,9 +192,12 @@ def cuda() -> C.CDLL:
         L.p2m_last_timings.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
         L.p2m_kernels_per_query.argtypes = [vp, C.c_uint64, C.POINTER(C.c_int)]
         L.p2m_set_scan_mode.argtypes = [vp, C.c_int]
-        L.p2m_set_nns_strategy.argtypes = [vp, C.c_int]
-        L.p2m_build_device.argtypes = [dp, C.c_uint64, u32p, C.c_uint64, C.POINTER(BuildConfig), C.c_int, C.POINTER(vp)]
-        L.p2m_table_job_device.argtypes = [vp, vp, u64p, C.POINTER(u32p)]
+        for name, at in (("p2m_set_nns_strategy", [vp, C.c_int]),
+                         ("p2m_build_device", [dp, C.c_uint64, u32p, C.c_uint64, C.POINTER(BuildConfig), C.c_int,
+                                               C.POINTER(vp)]),
+                         ("p2m_table_job_device", [vp, vp, u64p, C.POINTER(u32p)])):
+            if hasattr(L, name):  # absent only in A/B builds of older sources (scripts/gpu_ab.sh)
+                getattr(L, name).argtypes = at
         _cuda = L
     return _cuda
 

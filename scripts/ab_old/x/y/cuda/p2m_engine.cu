@@ -1,0 +1,999 @@
+// p2m_engine.cu -- the device engine behind the C ABI (include/p2m.h): packs the built structure
+// into the device layout, uploads it to the first GPU, replicates it to the others by a one-time
+// peer copy, and runs the query pipeline (Morton keys -> CUB radix sort -> fused query kernel).
+//
+// Multi-GPU: queries are independent (REF/SPEC.md:518-519), so p2m_query shards
+// rows evenly over the engine's devices, one host thread per device, with no collective on the hot
+// path; counters are summed on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../../include/p2m.h"
+#include "p2m_device.cuh"
+#include "p2m_kernels.cuh"
+
+#define P2M_API extern "C" __attribute__((visibility("default")))
+
+extern "C" void p2m_set_last_error_internal(const char* msg);  // libp2m_host.so
+
+using p2m::dev::D4;
+using p2m::dev::Params;
+
+namespace {
+
+void set_err(const std::string& s) { p2m_set_last_error_internal(s.c_str()); }
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) {                                                                 \
+            set_err(std::string(#x) + ": " + cudaGetErrorString(e_));                            \
+            return P2M_ERR_CUDA;                                                                 \
+        }                                                                                        \
+    } while (0)
+
+// ---- host-side packing --------------------------------------------------------------------
+
+uint64_t lb_left_size(uint64_t n) {
+    if (n <= 1) return 0;
+    int d = 63 - __builtin_clzll(n);
+    uint64_t full = (1ull << d) - 1ull, last = n - full, half = 1ull << (d - 1);
+    return (half - 1ull) + std::min(last, half);
+}
+
+// Left-balanced k-d tree in BFS order: split on the widest axis of the subset's box (lowest axis on
+// ties), the left subtree takes the lb_left_size(m) smallest points under (coordinate, site id).
+// Same definition as the oracle's tree (oracle/p2m_oracle.c orc_kdtree_build).
+void build_kdtree(const double* xyz, uint64_t n, std::vector<uint32_t>& node_site, std::vector<uint8_t>& node_dim) {
+    node_site.assign(n, 0);
+    node_dim.assign(n, 0);
+    std::vector<uint32_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0u);
+    struct T { uint64_t lo, hi, node; };
+    std::vector<T> st;
+    if (n) st.push_back({0, n, 0});
+    while (!st.empty()) {
+        T t = st.back();
+        st.pop_back();
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (uint64_t i = t.lo; i < t.hi; ++i)
+            for (int k = 0; k < 3; ++k) {
+                double v = xyz[3 * (uint64_t)idx[i] + k];
+                lo[k] = std::min(lo[k], v);
+                hi[k] = std::max(hi[k], v);
+            }
+        int dim = 0;
+        double ext = hi[0] - lo[0];
+        if (hi[1] - lo[1] > ext) { dim = 1; ext = hi[1] - lo[1]; }
+        if (hi[2] - lo[2] > ext) dim = 2;
+        const uint64_t m = t.hi - t.lo, l = lb_left_size(m);
+        std::nth_element(idx.begin() + t.lo, idx.begin() + t.lo + l, idx.begin() + t.hi, [&](uint32_t a, uint32_t b) {
+            double ka = xyz[3 * (uint64_t)a + dim], kb = xyz[3 * (uint64_t)b + dim];
+            return ka < kb || (ka == kb && a < b);
+        });
+        node_site[t.node] = idx[t.lo + l];
+        node_dim[t.node] = (uint8_t)dim;
+        if (t.hi > t.lo + l + 1) st.push_back({t.lo + l + 1, t.hi, 2 * t.node + 2});
+        if (l > 0) st.push_back({t.lo, t.lo + l, 2 * t.node + 1});
+    }
+}
+
+inline double bits_to_double(uint64_t b) { double d; std::memcpy(&d, &b, 8); return d; }
+
+// Fallback BVH: median split of centroids on the longest centroid-box axis, leaf 4, DFS order.
+struct FlatBvh {
+    std::vector<D4> nodes;     // 2 per node
+    std::vector<uint32_t> perm;
+};
+
+void build_bvh(const double* tri, uint64_t nf, FlatBvh& out) {
+    out.nodes.clear();
+    out.perm.resize(nf);
+    std::iota(out.perm.begin(), out.perm.end(), 0u);
+    if (!nf) return;
+    std::vector<double> cen(3 * nf);
+    for (uint64_t f = 0; f < nf; ++f)
+        for (int k = 0; k < 3; ++k) cen[3 * f + k] = (tri[9 * f + k] + tri[9 * f + 3 + k] + tri[9 * f + 6 + k]) * (1.0 / 3.0);
+    struct Rec {
+        FlatBvh& o; const double* tri; const std::vector<double>& cen;
+        uint32_t go(uint32_t lo, uint32_t hi) {
+            uint32_t me = (uint32_t)(o.nodes.size() / 2);
+            o.nodes.push_back(D4{}); o.nodes.push_back(D4{});
+            double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+            double cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (uint32_t i = lo; i < hi; ++i) {
+                uint32_t f = o.perm[i];
+                for (int v = 0; v < 3; ++v)
+                    for (int k = 0; k < 3; ++k) {
+                        double x = tri[9 * (uint64_t)f + 3 * v + k];
+                        bl[k] = std::min(bl[k], x); bh[k] = std::max(bh[k], x);
+                    }
+                for (int k = 0; k < 3; ++k) { cl[k] = std::min(cl[k], cen[3 * (uint64_t)f + k]); ch[k] = std::max(ch[k], cen[3 * (uint64_t)f + k]); }
+            }
+            uint64_t meta;
+            if (hi - lo <= 4) {
+                meta = (uint64_t)(hi - lo) << 32 | lo;
+            } else {
+                int ax = 0;
+                if (ch[1] - cl[1] > ch[ax] - cl[ax]) ax = 1;
+                if (ch[2] - cl[2] > ch[ax] - cl[ax]) ax = 2;
+                uint32_t mid = lo + (hi - lo) / 2;
+                std::nth_element(o.perm.begin() + lo, o.perm.begin() + mid, o.perm.begin() + hi, [&](uint32_t a, uint32_t b) {
+                    double x = cen[3 * (uint64_t)a + ax], y = cen[3 * (uint64_t)b + ax];
+                    return x < y || (x == y && a < b);
+                });
+                go(lo, mid);
+                uint32_t r = go(mid, hi);
+                meta = r;
+            }
+            o.nodes[2 * me] = D4{bl[0], bl[1], bl[2], bh[0]};
+            o.nodes[2 * me + 1] = D4{bh[1], bh[2], bits_to_double(meta), 0.0};
+            return me;
+        }
+    } rec{out, tri, cen};
+    rec.go(0, (uint32_t)nf);
+}
+
+struct Slot {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
+    float4* f32 = nullptr;
+    float4* bsph = nullptr;
+    float4* lbr = nullptr;
+    uint64_t* boff = nullptr;
+    uint64_t* off = nullptr;
+    uint32_t *lf = nullptr, *bvh_perm = nullptr;
+    uint8_t* heavy = nullptr;
+    D4* site_pos = nullptr;
+    D4* site_ref = nullptr;
+    uint32_t *grid_off = nullptr, *grid_site = nullptr;
+    Params params{};
+    std::mutex mu;
+    // host-API path: kPipe streams, each with a chunk-sized staging set, so the H2D copy of one
+    // chunk, the kernels of another and the D2H copy of a third overlap
+    static constexpr int kPipe = 4;
+    cudaStream_t pipe[kPipe] = {};
+    struct Ws {
+        double *q = nullptr, *dist = nullptr, *cp = nullptr;
+        uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
+    } ws[kPipe];
+    uint64_t cap = 0;
+    cudaEvent_t agg_ready = nullptr;
+    unsigned long long* agg = nullptr;
+    // profiling: ring of event sets, read lazily by p2m_last_timings (no host sync per call)
+    static constexpr int kRing = 256;
+    static constexpr int kEv = 6;  // morton | sort | descend | regroup sort | scan | end
+    std::vector<cudaEvent_t> ev;   // kEv per ring entry
+    int recorded = 0;
+};
+
+}  // namespace
+
+struct p2m_engine {
+    std::vector<std::unique_ptr<Slot>> slots;
+    double replicate_ms = 0.0;
+    uint64_t bytes = 0;
+    bool profiling = false;
+    int scan_mode = P2M_SCAN_GROUPED;
+    int e2e_chunks = 4;  // host-buffer path pipeline depth (P2M_E2E_CHUNKS overrides)
+    uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
+    uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
+    uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
+};
+
+namespace {
+
+void free_slot(Slot& s) {
+    cudaSetDevice(s.dev);
+    cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
+    cudaFree(s.heavy);
+    cudaFree(s.site_pos); cudaFree(s.site_ref); cudaFree(s.grid_off); cudaFree(s.grid_site);
+    cudaFree(s.f32);
+    cudaFree(s.bsph); cudaFree(s.boff); cudaFree(s.lbr);
+    for (auto& w : s.ws) {
+        cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
+    }
+    for (auto& st : s.pipe) if (st) cudaStreamDestroy(st);
+    if (s.agg_ready) cudaEventDestroy(s.agg_ready);
+    cudaFree(s.agg);
+    for (auto& e : s.ev) if (e) cudaEventDestroy(e);
+    s.ev.clear();
+    if (s.stream) cudaStreamDestroy(s.stream);
+}
+
+// Exact cell-locate grid over the Morton key box (1.5x the real sites' AABB): cubic cells, about 16
+// per real site, at most 512 per axis; site s is listed in every cell its Voronoi cell box (inflated
+// by 1e-9 |D|) meets.  Built only when (1) every real site has a box and (2) no sentinel can be
+// nearest anywhere in the grid box: with s0 the real site nearest the box centre, every point x of
+// the box has d(x, nearest real) <= max_corner |corner - s0| < min_k d(sentinel_k, box).
+struct Grid {
+    double lo[3] = {0, 0, 0}, inv[3] = {0, 0, 0};
+    uint32_t res[3] = {0, 0, 0};
+    std::vector<uint32_t> off, site;
+};
+
+bool build_grid(const p2m_engine_desc* d, const double* key_lo, const double* key_ext, Grid& g) {
+    if (!d->site_cell_box) return false;
+    const uint64_t S = d->n_sites;
+    double hi[3], c[3];
+    for (int k = 0; k < 3; ++k) { hi[k] = key_lo[k] + key_ext[k]; c[k] = 0.5 * (key_lo[k] + hi[k]); }
+    uint64_t n_real = 0, s0 = UINT64_MAX;
+    double best = INFINITY;
+    for (uint64_t s = 0; s < S; ++s) {
+        if (d->site_kind[s] == P2M_SITE_SENTINEL) continue;
+        ++n_real;
+        const double* b = d->site_cell_box + 6 * s;
+        for (int k = 0; k < 6; ++k) if (!std::isfinite(b[k])) return false;
+        const double* p = d->site_xyz + 3 * s;
+        const double dd = (p[0] - c[0]) * (p[0] - c[0]) + (p[1] - c[1]) * (p[1] - c[1]) + (p[2] - c[2]) * (p[2] - c[2]);
+        if (dd < best) { best = dd; s0 = s; }
+    }
+    if (!n_real) return false;
+    double rmax = 0.0;
+    for (int i = 0; i < 8; ++i) {
+        double dd = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double x = (i >> k & 1) ? hi[k] : key_lo[k];
+            dd += (x - d->site_xyz[3 * s0 + k]) * (x - d->site_xyz[3 * s0 + k]);
+        }
+        rmax = std::max(rmax, std::sqrt(dd));
+    }
+    for (uint64_t s = 0; s < S; ++s) {
+        if (d->site_kind[s] != P2M_SITE_SENTINEL) continue;
+        double dd = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            const double x = d->site_xyz[3 * s + k];
+            const double t = x < key_lo[k] ? key_lo[k] - x : (x > hi[k] ? x - hi[k] : 0.0);
+            dd += t * t;
+        }
+        if (!(std::sqrt(dd) > rmax * (1.0 + 1e-9))) return false;
+    }
+    const double vol = key_ext[0] * key_ext[1] * key_ext[2];
+    const double cell = std::cbrt(vol / (16.0 * (double)n_real));
+    for (int k = 0; k < 3; ++k) {
+        g.lo[k] = key_lo[k];
+        g.res[k] = (uint32_t)std::min(512.0, std::max(1.0, std::ceil(key_ext[k] / cell)));
+        g.inv[k] = (double)g.res[k] / key_ext[k];
+    }
+    double dspan = 0.0;
+    for (int k = 0; k < 3; ++k) dspan += (d->domain_max[k] - d->domain_min[k]) * (d->domain_max[k] - d->domain_min[k]);
+    const double margin = 1e-9 * std::sqrt(dspan);
+    const uint64_t ncell = (uint64_t)g.res[0] * g.res[1] * g.res[2];
+    auto range = [&](const double* b, uint32_t* i0, uint32_t* i1) {
+        for (int k = 0; k < 3; ++k) {
+            const double a = (b[k] - margin - g.lo[k]) * g.inv[k], z = (b[3 + k] + margin - g.lo[k]) * g.inv[k];
+            if (z < 0.0 || a >= (double)g.res[k]) return false;
+            i0[k] = a <= 0.0 ? 0u : (uint32_t)std::min<double>(std::floor(a), g.res[k] - 1);
+            i1[k] = z <= 0.0 ? 0u : (uint32_t)std::min<double>(std::floor(z), g.res[k] - 1);
+        }
+        return true;
+    };
+    std::vector<uint64_t> cnt(ncell + 1, 0);
+    uint32_t i0[3], i1[3];
+    for (int pass = 0; pass < 2; ++pass) {
+        std::vector<uint64_t> cur;
+        if (pass == 1) {
+            for (uint64_t cidx = 0; cidx < ncell; ++cidx) cnt[cidx + 1] += cnt[cidx];
+            if (cnt[ncell] >= (1ull << 32)) return false;
+            g.site.resize(cnt[ncell]);
+            cur.assign(cnt.begin(), cnt.end() - 1);
+        }
+        for (uint64_t s = 0; s < S; ++s) {
+            if (d->site_kind[s] == P2M_SITE_SENTINEL) continue;
+            if (!range(d->site_cell_box + 6 * s, i0, i1)) continue;
+            for (uint32_t z = i0[2]; z <= i1[2]; ++z)
+                for (uint32_t y = i0[1]; y <= i1[1]; ++y)
+                    for (uint32_t x = i0[0]; x <= i1[0]; ++x) {
+                        const uint64_t cidx = ((uint64_t)z * g.res[1] + y) * g.res[0] + x;
+                        if (pass == 0) ++cnt[cidx + 1];
+                        else g.site[cur[cidx]++] = (uint32_t)s;
+                    }
+        }
+    }
+    g.off.resize(ncell + 1);
+    for (uint64_t cidx = 0; cidx <= ncell; ++cidx) g.off[cidx] = (uint32_t)cnt[cidx];
+    return true;
+}
+
+int alloc_slot(Slot& s, const p2m_engine& E) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    for (auto& st : s.pipe) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s.agg_ready, cudaEventDisableTiming));
+    CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.bsph, sizeof(float4) * std::max<uint64_t>(1, E.n_batches)));
+    CK(cudaMalloc(&s.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.boff, sizeof(uint64_t) * (E.n_sites + 1)));
+    CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
+    CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
+    CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
+    CK(cudaMalloc(&s.bvh_perm, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.agg, sizeof(unsigned long long) * 8));
+    CK(cudaMalloc(&s.heavy, std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMalloc(&s.site_pos, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    CK(cudaMalloc(&s.site_ref, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    if (E.grid_cells) {
+        CK(cudaMalloc(&s.grid_off, 4 * (E.grid_cells + 1)));
+        CK(cudaMalloc(&s.grid_site, 4 * std::max<uint64_t>(1, E.grid_pairs)));
+    }
+    CK(cudaMemset(s.heavy, 0, std::max<uint64_t>(1, E.n_sites)));
+    s.ev.assign(Slot::kEv * Slot::kRing, nullptr);
+    for (auto& e : s.ev) CK(cudaEventCreate(&e));
+    // keep the stream-ordered pool's memory between calls (the per-call sort workspace)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, s.dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return P2M_OK;
+}
+
+int ensure_ws(Slot& s, uint64_t n) {
+    if (n <= s.cap) return P2M_OK;
+    CK(cudaDeviceSynchronize());
+    s.cap = 0;
+    for (auto& w : s.ws) {
+        cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
+        w = Slot::Ws{};
+        CK(cudaMalloc(&w.q, 24 * n));
+        CK(cudaMalloc(&w.dist, 8 * n));
+        CK(cudaMalloc(&w.cp, 24 * n));
+        CK(cudaMalloc(&w.face, 4 * n));
+        CK(cudaMalloc(&w.site, 4 * n));
+        CK(cudaMalloc(&w.flags, 4 * n));
+    }
+    s.cap = n;
+    return P2M_OK;
+}
+
+// Morton keys -> sort -> fused query.  rows_out (optional) receives the sorted row order.
+int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2m::dev::Out& o, bool counters,
+                 cudaStream_t st, bool nearest_only, uint32_t* d_site_only, bool allow_prof = true) {
+    if (n >= (1ull << 32)) { set_err("p2m_query_device: at most 2^32-1 rows per call"); return P2M_ERR_INVALID; }
+    CK(cudaSetDevice(s.dev));
+    uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
+    void* tmp = nullptr;
+    uint32_t *flag = nullptr, *tix = nullptr, *tiles = nullptr, *meta = nullptr;
+    const bool grouped = !nearest_only && E->scan_mode == P2M_SCAN_GROUPED;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
+    tb = std::max(tb, p2m::dev::tiles_tmp_bytes(n));
+    CK(cudaMallocAsync(&keys, 4 * n, st));
+    CK(cudaMallocAsync(&rows, 4 * n, st));
+    CK(cudaMallocAsync(&keys2, 4 * n, st));
+    CK(cudaMallocAsync(&rows2, 4 * n, st));
+    CK(cudaMallocAsync(&tmp, tb, st));
+    if (grouped) {
+        CK(cudaMallocAsync(&flag, 4 * n, st));
+        CK(cudaMallocAsync(&tix, 4 * n, st));
+        CK(cudaMallocAsync(&tiles, 4 * p2m::dev::max_tiles(n, E->n_sites), st));
+        CK(cudaMallocAsync(&meta, 16, st));
+    }
+    const bool prof = allow_prof && E->profiling && s.recorded < Slot::kRing;
+    cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * s.recorded] : nullptr;
+    if (prof) { CK(cudaEventRecord(ev[0], st)); ++s.recorded; }
+    CK(p2m::dev::launch_morton(d_q, n, s.params, keys, rows, st));
+    if (prof) CK(cudaEventRecord(ev[1], st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
+    if (prof) CK(cudaEventRecord(ev[2], st));
+    if (nearest_only) {
+        CK(p2m::dev::launch_nearest(s.params, d_q, rows2, n, d_site_only, st));
+        if (prof) for (int k = 3; k < Slot::kEv; ++k) CK(cudaEventRecord(ev[k], st));
+    } else if (E->scan_mode == P2M_SCAN_FUSED) {
+        CK(p2m::dev::launch_query(s.params, d_q, rows2, n, o, counters, st));
+        if (prof) for (int k = 3; k < Slot::kEv; ++k) CK(cudaEventRecord(ev[k], st));
+    } else {
+        // descend in Morton order (keys buffer reused for the site keys), regroup by site (stable),
+        // then scan per site tile
+        CK(p2m::dev::launch_descend(s.params, d_q, rows2, n, keys, o, counters, st));
+        if (prof) CK(cudaEventRecord(ev[3], st));
+        const int bits = std::max(1, 64 - __builtin_clzll((unsigned long long)E->n_sites));  // keys <= n_sites
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows2, rows, (int64_t)n, 0, bits, st));
+        // tiles over the site-sorted order (keys / rows2 are free again: hpos / run starts)
+        CK(p2m::dev::launch_tiles(s.params, keys2, n, (uint32_t)E->n_sites, keys, rows2, flag, tix, tiles, meta, tmp, tb, st));
+        if (prof) CK(cudaEventRecord(ev[4], st));
+        CK(p2m::dev::launch_scan_tiles(s.params, d_q, rows, keys2, tiles, meta, n, o, counters, st));
+        if (prof) CK(cudaEventRecord(ev[5], st));
+    }
+    CK(cudaFreeAsync(keys, st));
+    CK(cudaFreeAsync(rows, st));
+    CK(cudaFreeAsync(keys2, st));
+    CK(cudaFreeAsync(rows2, st));
+    CK(cudaFreeAsync(tmp, st));
+    if (grouped) {
+        CK(cudaFreeAsync(flag, st));
+        CK(cudaFreeAsync(tix, st));
+        CK(cudaFreeAsync(tiles, st));
+        CK(cudaFreeAsync(meta, st));
+    }
+    return P2M_OK;
+}
+
+// Per-site exact-work estimate: query every site's own position once with the sequential (fused)
+// scan and count the exact point-triangle evaluations.  Sites whose estimate reaches the threshold
+// (deep auxiliary sites of closed surfaces, where the distance field is flat and sphere pruning
+// cannot cut the list) get short tiles so their rows spread over many SMs.
+int mark_heavy_sites(p2m_engine* E, const p2m_engine_desc* d) {
+    uint32_t thr = 1024;
+    if (const char* v = std::getenv("P2M_HEAVY_E")) thr = (uint32_t)std::strtoul(v, nullptr, 10);
+    const uint64_t S = E->n_sites;
+    Slot& s0 = *E->slots[0];
+    CK(cudaSetDevice(s0.dev));
+    double *q = nullptr, *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr;
+    uint64_t* pq = nullptr;
+    CK(cudaMalloc(&q, 24 * S)); CK(cudaMalloc(&dist, 8 * S)); CK(cudaMalloc(&cp, 24 * S));
+    CK(cudaMalloc(&face, 4 * S)); CK(cudaMalloc(&site, 4 * S)); CK(cudaMalloc(&pq, 24 * S));
+    CK(cudaMemcpy(q, d->site_xyz, 24 * S, cudaMemcpyHostToDevice));
+    const int mode = E->scan_mode;
+    const bool prof = E->profiling;
+    E->scan_mode = P2M_SCAN_FUSED;
+    E->profiling = false;
+    p2m::dev::Out o{dist, cp, face, site, nullptr, pq, nullptr};
+    int rc = run_pipeline(E, s0, q, S, o, true, s0.stream, false, nullptr);
+    E->scan_mode = mode;
+    E->profiling = prof;
+    std::vector<uint64_t> h(3 * S);
+    if (rc == P2M_OK) {
+        CK(cudaStreamSynchronize(s0.stream));
+        CK(cudaMemcpy(h.data(), pq, 24 * S, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(q); cudaFree(dist); cudaFree(cp); cudaFree(face); cudaFree(site); cudaFree(pq);
+    if (rc != P2M_OK) return rc;
+    std::vector<uint8_t> heavy(S, 0);
+    uint64_t n_heavy = 0;
+    for (uint64_t i = 0; i < S; ++i)
+        if (d->site_kind[i] != P2M_SITE_SENTINEL && h[3 * i + 1] >= thr) { heavy[i] = 1; ++n_heavy; }
+    E->n_heavy = n_heavy;
+    for (auto& s : E->slots) {
+        CK(cudaSetDevice(s->dev));
+        CK(cudaMemcpy(s->heavy, heavy.data(), S, cudaMemcpyHostToDevice));
+    }
+    return P2M_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+
+P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int* device_ids, p2m_engine** out) {
+    if (!d || !out || n_devices < 1 || !d->site_xyz || !d->site_kind || !d->tri_xyz || !d->face_sphere ||
+        !d->list_offsets || (!d->list_faces && d->list_offsets[d->n_sites] > 0)) {
+        set_err("p2m_engine_create: invalid descriptor");
+        return P2M_ERR_INVALID;
+    }
+    if (d->n_sites == 0 || d->n_faces == 0 || d->n_sites >= (1ull << 32) || d->n_faces >= (1ull << 32)) {
+        set_err("p2m_engine_create: engine not built (no sites/faces) or too large");
+        return P2M_ERR_NOT_BUILT;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        set_err("p2m_engine_create: no CUDA device available");
+        return P2M_ERR_CUDA;
+    }
+    const uint64_t S = d->n_sites, F = d->n_faces, L = d->list_offsets[S];
+    for (uint64_t s = 0; s < S; ++s)
+        if (d->list_offsets[s] > d->list_offsets[s + 1]) { set_err("p2m_engine_create: offsets not monotone"); return P2M_ERR_INVALID; }
+    for (uint64_t j = 0; j < L; ++j)
+        if (d->list_faces[j] >= F) { set_err("p2m_engine_create: list face id out of range"); return P2M_ERR_INVALID; }
+
+    auto E = std::make_unique<p2m_engine>();
+    E->n_sites = S; E->n_faces = F; E->n_entries = L;
+
+    // ---- pack ----
+    std::vector<uint32_t> node_site;
+    std::vector<uint8_t> node_dim;
+    build_kdtree(d->site_xyz, S, node_site, node_dim);
+    std::vector<D4> kd(S);
+    double klo[3] = {INFINITY, INFINITY, INFINITY}, khi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint64_t k = 0; k < S; ++k) {
+        const uint32_t id = node_site[k];
+        const double* p = d->site_xyz + 3 * (uint64_t)id;
+        uint64_t meta = (uint64_t)id | (uint64_t)node_dim[k] << 32 |
+                        (d->site_kind[id] == P2M_SITE_SENTINEL ? (1ull << 34) : 0ull);
+        kd[k] = D4{p[0], p[1], p[2], bits_to_double(meta)};
+        if (d->site_kind[id] != P2M_SITE_SENTINEL)
+            for (int c = 0; c < 3; ++c) { klo[c] = std::min(klo[c], p[c]); khi[c] = std::max(khi[c], p[c]); }
+    }
+    std::vector<D4> rec(4 * F);
+    for (uint64_t f = 0; f < F; ++f) {
+        const double* t = d->tri_xyz + 9 * f;
+        const double* s = d->face_sphere + 4 * f;
+        rec[4 * f] = D4{s[0], s[1], s[2], s[3]};
+        rec[4 * f + 1] = D4{t[0], t[1], t[2], t[3]};
+        rec[4 * f + 2] = D4{t[4], t[5], t[6], t[7]};
+        // padding of the last sector: the face's unit normal in fp32 (for the plane-distance bound)
+        const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+        const double vx = t[6] - t[0], vy = t[7] - t[1], vz = t[8] - t[2];
+        double nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
+        const double nl = std::sqrt(nx * nx + ny * ny + nz * nz);
+        if (nl > 0.0 && std::isfinite(nl)) { nx /= nl; ny /= nl; nz /= nl; } else { nx = ny = nz = 0.0; }
+        const float fn[4] = {(float)nx, (float)ny, (float)nz, 0.0f};
+        double p0, p1;
+        std::memcpy(&p0, fn, 8);
+        std::memcpy(&p1, fn + 2, 8);
+        rec[4 * f + 3] = D4{t[8], p0, p1, 0.0};
+    }
+    // fp32 pre-filter records (k_scan_tiles): centre rounded to nearest, radius rounded up and
+    // multiplied by K = 1.000001 rounding up -- the same values the kernel's bound assumes
+    std::vector<float4> f32(F);
+    for (uint64_t f = 0; f < F; ++f) {
+        const double* sp = d->face_sphere + 4 * f;
+        float r = (float)sp[3];
+        if ((double)r < sp[3]) r = std::nextafter(r, INFINITY);
+        const double prod = (double)r * (double)1.000001f;
+        float rk = (float)prod;
+        if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
+        f32[f] = make_float4((float)sp[0], (float)sp[1], (float)sp[2], rk);
+    }
+    // level-1 pruning spheres: one per aligned 32-entry batch of every list.  Centre = centre of the
+    // members' sphere boxes; radius = max |c_i - C| + r_i, then made conservative for the fp32
+    // kernel test (centre rounded to nearest, radius grown by the centre's rounding and rounded up,
+    // times K rounded up -- the same form as the per-face records)
+    std::vector<uint64_t> boff(S + 1, 0);
+    for (uint64_t s = 0; s < S; ++s) boff[s + 1] = boff[s] + (d->list_offsets[s + 1] - d->list_offsets[s] + 31) / 32;
+    E->n_batches = boff[S];
+    std::vector<float4> bsph(std::max<uint64_t>(1, E->n_batches));
+    for (uint64_t s = 0; s < S; ++s) {
+        const uint64_t b0 = d->list_offsets[s], b1 = d->list_offsets[s + 1];
+        for (uint64_t j = b0, bi = boff[s]; j < b1; j += 32, ++bi) {
+            const uint64_t je = std::min(b1, j + 32);
+            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (uint64_t t = j; t < je; ++t) {
+                const double* sp = d->face_sphere + 4 * (uint64_t)d->list_faces[t];
+                for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], sp[k] - sp[3]); hi[k] = std::max(hi[k], sp[k] + sp[3]); }
+            }
+            double C[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+            float cf[3] = {(float)C[0], (float)C[1], (float)C[2]};
+            double R = 0.0;
+            for (uint64_t t = j; t < je; ++t) {
+                const double* sp = d->face_sphere + 4 * (uint64_t)d->list_faces[t];
+                double dd = 0.0;
+                for (int k = 0; k < 3; ++k) dd += (sp[k] - (double)cf[k]) * (sp[k] - (double)cf[k]);
+                R = std::max(R, std::sqrt(dd) + sp[3]);
+            }
+            R = R * (1.0 + 1e-12) + 1e-300;
+            float rf = (float)R;
+            if ((double)rf < R) rf = std::nextafter(rf, INFINITY);
+            const double prod = (double)rf * (double)1.000001f;
+            float rk = (float)prod;
+            if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
+            bsph[bi] = make_float4(cf[0], cf[1], cf[2], rk);
+        }
+    }
+    // tight fp32 lower-bound records (k_scan_tiles rare path): d(q,T)^2 >= h^2 + max(0, s_i)^2 with
+    // h = n.(q-a) and s_i the signed in-plane distances to the three edge lines (outward positive)
+    std::vector<float4> lbr(4 * std::max<uint64_t>(1, F));
+    for (uint64_t f = 0; f < F; ++f) {
+        const double* t = d->tri_xyz + 9 * f;
+        const double A[3] = {t[0], t[1], t[2]}, B[3] = {t[3], t[4], t[5]}, Cc[3] = {t[6], t[7], t[8]};
+        auto sub3 = [](const double* x, const double* y, double* o) { for (int k = 0; k < 3; ++k) o[k] = x[k] - y[k]; };
+        auto crs = [](const double* x, const double* y, double* o) {
+            o[0] = x[1] * y[2] - x[2] * y[1]; o[1] = x[2] * y[0] - x[0] * y[2]; o[2] = x[0] * y[1] - x[1] * y[0];
+        };
+        auto unit = [](double* v) {
+            const double l = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            if (l > 0.0 && std::isfinite(l)) { v[0] /= l; v[1] /= l; v[2] /= l; return true; }
+            v[0] = v[1] = v[2] = 0.0;
+            return false;
+        };
+        double ab[3], ac[3], bc[3], ca[3], n[3], m1[3], m2[3], m3[3];
+        sub3(B, A, ab); sub3(Cc, A, ac); sub3(Cc, B, bc); sub3(A, Cc, ca);
+        crs(ab, ac, n);
+        bool ok = unit(n);
+        crs(ab, n, m1); crs(bc, n, m2); crs(ca, n, m3);
+        ok = ok && unit(m1) && unit(m2) && unit(m3);
+        if (!ok) { for (int k = 0; k < 3; ++k) n[k] = m1[k] = m2[k] = m3[k] = 0.0; }  // never prunes
+        const double o2 = ok ? (m2[0] * ab[0] + m2[1] * ab[1] + m2[2] * ab[2]) : 0.0;
+        lbr[4 * f] = make_float4((float)A[0], (float)A[1], (float)A[2], (float)n[0]);
+        lbr[4 * f + 1] = make_float4((float)n[1], (float)n[2], (float)m1[0], (float)m1[1]);
+        lbr[4 * f + 2] = make_float4((float)m1[2], (float)m2[0], (float)m2[1], (float)m2[2]);
+        lbr[4 * f + 3] = make_float4((float)m3[0], (float)m3[1], (float)m3[2], (float)o2);
+    }
+    FlatBvh bvh;
+    build_bvh(d->tri_xyz, F, bvh);
+    E->n_bvh = bvh.nodes.size() / 2;
+
+    Params P{};
+    P.n_nodes = (uint32_t)S;
+    P.n_faces = (uint32_t)F;
+    double dd2 = 0.0;
+    {
+        double dx = d->domain_max[0] - d->domain_min[0], dy = d->domain_max[1] - d->domain_min[1],
+               dz = d->domain_max[2] - d->domain_min[2];
+        dd2 = dx * dx + dy * dy + dz * dz;
+    }
+    P.prune_eps = 1e-9 * std::sqrt(dd2);  // same definition as the oracle (orc_ctx_create)
+    {
+        // fp32 pre-filter slack: coordinates of every scanned query and sphere centre lie in D, so
+        // rounding each to fp32 moves |q - c| by at most 2*sqrt(3)*2^-24*M; doubled, plus 2 eps
+        double M = 0.0;
+        for (int c = 0; c < 3; ++c) M = std::max({M, std::fabs(d->domain_min[c]), std::fabs(d->domain_max[c])});
+        const double delta = 4.0 * std::sqrt(3.0) * std::ldexp(1.0, -24) * M + 2.0 * P.prune_eps;
+        float df = (float)delta;
+        if ((double)df < delta) df = std::nextafter(df, INFINITY);
+        P.f32_delta = df;
+        // lower-bound record error: each dot product of a unit vector with fl(q_f - a_f) is within
+        // ~25*2^-24*M of exact, the edge offset adds ~4*2^-24*M; 64*2^-24*M covers both with margin
+        const double lm = 64.0 * std::ldexp(1.0, -24) * M;
+        float lmf = (float)lm;
+        if ((double)lmf < lm) lmf = std::nextafter(lmf, INFINITY);
+        P.lb_margin = lmf;
+    }
+    P.long_tile = 32;
+    if (const char* v = std::getenv("P2M_LONG_TILE")) {
+        uint32_t t = (uint32_t)std::strtoul(v, nullptr, 10);
+        if (t == 32 || t == 64 || t == 128 || t == 256) P.long_tile = t;
+    }
+    double kext[3] = {0, 0, 0};  // Morton key box = cell-locate grid box extents
+    for (int c = 0; c < 3; ++c) {
+        P.dmin[c] = d->domain_min[c];
+        P.dmax[c] = d->domain_max[c];
+        if (!(klo[c] <= khi[c])) { klo[c] = d->domain_min[c]; khi[c] = d->domain_max[c]; }
+        double mid = 0.5 * (klo[c] + khi[c]), h = 0.75 * (khi[c] - klo[c]);  // = builder.cpp gbox
+        if (!(h > 0)) h = 1.0;
+        P.key_lo[c] = mid - h;
+        P.key_scale[c] = 1024.0 / (2.0 * h);
+        kext[c] = 2.0 * h;
+    }
+
+    Grid grid;
+    {
+        double ext[3];
+        for (int c = 0; c < 3; ++c) ext[c] = kext[c];
+        if (build_grid(d, P.key_lo, ext, grid)) {
+            E->grid_cells = (uint64_t)grid.res[0] * grid.res[1] * grid.res[2];
+            E->grid_pairs = grid.site.size();
+            for (int c = 0; c < 3; ++c) { P.grid_lo[c] = grid.lo[c]; P.grid_inv[c] = grid.inv[c]; P.grid_res[c] = grid.res[c]; }
+        }
+        if (std::getenv("P2M_NO_GRID")) E->grid_cells = E->grid_pairs = 0;
+        P.no_seed = std::getenv("P2M_NO_SEED") ? 1 : 0;
+        P.no_batch = std::getenv("P2M_NO_BATCH") ? 1 : 0;
+    }
+    std::vector<D4> site_pos(S), site_ref(S);
+    for (uint64_t i = 0; i < S; ++i) {
+        const double* x = d->site_xyz + 3 * i;
+        site_pos[i] = D4{x[0], x[1], x[2], bits_to_double(d->site_kind[i] == P2M_SITE_SENTINEL ? (1ull << 34) : 0ull)};
+        // a point on the mesh for the d_min seed: the vertex itself, or the auxiliary projection
+        site_ref[i] = D4{0.0, 0.0, 0.0, 0.0};
+        if (d->site_kind[i] == P2M_SITE_MESH_VERTEX) {
+            site_ref[i] = D4{x[0], x[1], x[2], 1.0};
+        } else if (d->site_kind[i] == P2M_SITE_AUXILIARY && d->site_ref_xyz) {
+            const double* r = d->site_ref_xyz + 3 * i;
+            if (std::isfinite(r[0]) && std::isfinite(r[1]) && std::isfinite(r[2])) site_ref[i] = D4{r[0], r[1], r[2], 1.0};
+        }
+    }
+    // ---- upload to the first device, peer-replicate to the rest ----
+    for (int k = 0; k < n_devices; ++k) {
+        auto s = std::make_unique<Slot>();
+        s->dev = device_ids ? device_ids[k] : k;
+        if (s->dev < 0 || s->dev >= ndev) { set_err("p2m_engine_create: bad device id"); return P2M_ERR_INVALID; }
+        E->slots.push_back(std::move(s));
+    }
+    for (auto& s : E->slots) {
+        int rc = alloc_slot(*s, *E);
+        if (rc != P2M_OK) { for (auto& x : E->slots) free_slot(*x); return rc; }
+    }
+    Slot& s0 = *E->slots[0];
+    auto fail = [&](int rc) { for (auto& x : E->slots) free_slot(*x); return rc; };
+    {
+        cudaSetDevice(s0.dev);
+        if (cudaMemcpy(s0.kd, kd.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.rec, rec.data(), sizeof(D4) * 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.f32, f32.data(), sizeof(float4) * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.bsph, bsph.data(), sizeof(float4) * bsph.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.boff, boff.data(), 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.lbr, lbr.data(), sizeof(float4) * lbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+            (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
+            cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.site_pos, site_pos.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.site_ref, site_ref.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            (E->grid_cells && cudaMemcpy(s0.grid_off, grid.off.data(), 4 * (E->grid_cells + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
+            (E->grid_pairs && cudaMemcpy(s0.grid_site, grid.site.data(), 4 * E->grid_pairs, cudaMemcpyHostToDevice) != cudaSuccess)) {
+            set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
+            return fail(P2M_ERR_CUDA);
+        }
+    }
+    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (5 * F + E->n_batches) + 8 * (S + 1) + 8 * (S + 1) + 4 * (L + F) + S +
+               (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0);
+    auto t0 = std::chrono::steady_clock::now();
+    for (size_t k = 1; k < E->slots.size(); ++k) {
+        Slot& s = *E->slots[k];
+        cudaSetDevice(s.dev);
+        if (s.dev != s0.dev) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, s.dev, s0.dev);
+            if (can) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(s0.dev, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) { set_err("peer access failed"); return fail(P2M_ERR_CUDA); }
+                cudaGetLastError();
+            }
+        }
+        struct { void* dst; const void* src; size_t n; } cp[] = {
+            {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
+            {s.bsph, s0.bsph, sizeof(float4) * std::max<uint64_t>(1, E->n_batches)}, {s.boff, s0.boff, 8 * (S + 1)},
+            {s.lbr, s0.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, F)},
+            {s.off, s0.off, 8 * (S + 1)},
+            {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
+            {s.site_pos, s0.site_pos, sizeof(D4) * S}, {s.site_ref, s0.site_ref, sizeof(D4) * S},
+            {s.grid_off, s0.grid_off, E->grid_cells ? 4 * (E->grid_cells + 1) : 0},
+            {s.grid_site, s0.grid_site, 4 * E->grid_pairs}};
+        for (auto& c : cp)
+            if (c.n && cudaMemcpyPeerAsync(c.dst, s.dev, c.src, s0.dev, c.n, s.stream) != cudaSuccess) {
+                set_err("p2m_engine_create: peer copy failed");
+                return fail(P2M_ERR_CUDA);
+            }
+    }
+    for (auto& s : E->slots) {
+        cudaSetDevice(s->dev);
+        if (cudaStreamSynchronize(s->stream) != cudaSuccess) { set_err("p2m_engine_create: replica sync failed"); return fail(P2M_ERR_CUDA); }
+    }
+    E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& s : E->slots) {
+        s->params = P;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.lbr = s->lbr; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
+        s->params.site_pos = s->site_pos;
+        s->params.site_ref = s->site_ref;
+        s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
+        s->params.grid_site = s->grid_site;
+    }
+    if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(1, std::atoi(v));
+    {
+        int rc = mark_heavy_sites(E.get(), d);
+        if (rc != P2M_OK) return fail(rc);
+    }
+    *out = E.release();
+    return P2M_OK;
+}
+
+P2M_API void p2m_engine_destroy(p2m_engine* e) {
+    if (!e) return;
+    for (auto& s : e->slots) free_slot(*s);
+    delete e;
+}
+
+P2M_API int p2m_engine_info(const p2m_engine* e, int* n, double* ms, uint64_t* bytes) {
+    if (!e) { set_err("p2m_engine_info: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (n) *n = (int)e->slots.size();
+    if (ms) *ms = e->replicate_ms;
+    if (bytes) *bytes = e->bytes;
+    return P2M_OK;
+}
+
+P2M_API int p2m_query_device(p2m_engine* e, int slot, const double* d_q, uint64_t n, double* d_dist, double* d_cp,
+                             uint32_t* d_face, uint32_t* d_site, uint32_t* d_flags, void* stream, p2m_counters* cnt) {
+    if (!e) { set_err("p2m_query_device: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (slot < 0 || slot >= (int)e->slots.size()) { set_err("p2m_query_device: bad slot"); return P2M_ERR_INVALID; }
+    if (n && (!d_q || !d_dist || !d_cp || !d_face || !d_site)) { set_err("p2m_query_device: null buffer"); return P2M_ERR_INVALID; }
+    Slot& s = *e->slots[slot];
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cnt) std::memset(cnt, 0, sizeof *cnt);
+    if (!n) return P2M_OK;
+    p2m::dev::Out o{d_dist, d_cp, d_face, d_site, d_flags, nullptr, nullptr};
+    std::unique_lock<std::mutex> lk(s.mu, std::defer_lock);
+    if (cnt) {
+        lk.lock();
+        CK(cudaSetDevice(s.dev));
+        CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, st));
+        o.agg = s.agg;
+    }
+    int rc = run_pipeline(e, s, d_q, n, o, cnt != nullptr, st, false, nullptr);
+    if (rc != P2M_OK) return rc;
+    if (cnt) {
+        unsigned long long h[8];
+        CK(cudaMemcpyAsync(h, s.agg, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cnt->n_queries = n;
+        cnt->candidates_visited = h[0];
+        cnt->exact_evaluations = h[1];
+        cnt->pruned = h[0] - h[1];
+        cnt->kd_nodes_visited = h[2];
+        cnt->filter_passes = h[4];
+        cnt->warp_rare_iters = h[5];
+        cnt->fallbacks = h[3];
+    }
+    return P2M_OK;
+}
+
+P2M_API int p2m_nearest_site_device(p2m_engine* e, int slot, const double* d_q, uint64_t n, uint32_t* d_site, void* stream) {
+    if (!e) { set_err("p2m_nearest_site_device: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (slot < 0 || slot >= (int)e->slots.size()) { set_err("bad slot"); return P2M_ERR_INVALID; }
+    if (!n) return P2M_OK;
+    p2m::dev::Out o{};
+    return run_pipeline(e, *e->slots[slot], d_q, n, o, false, (cudaStream_t)stream, true, d_site);
+}
+
+P2M_API int p2m_query_device_counters(p2m_engine* e, int slot, const double* d_q, uint64_t n, uint64_t* d_pq, void* stream) {
+    if (!e) { set_err("p2m_query_device_counters: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (slot < 0 || slot >= (int)e->slots.size()) { set_err("bad slot"); return P2M_ERR_INVALID; }
+    if (!n) return P2M_OK;
+    Slot& s = *e->slots[slot];
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaSetDevice(s.dev));
+    double *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr;
+    CK(cudaMallocAsync(&dist, 8 * n, st));
+    CK(cudaMallocAsync(&cp, 24 * n, st));
+    CK(cudaMallocAsync(&face, 4 * n, st));
+    CK(cudaMallocAsync(&site, 4 * n, st));
+    p2m::dev::Out o{dist, cp, face, site, nullptr, d_pq, nullptr};
+    int rc = run_pipeline(e, s, d_q, n, o, true, st, false, nullptr);
+    cudaFreeAsync(dist, st); cudaFreeAsync(cp, st); cudaFreeAsync(face, st); cudaFreeAsync(site, st);
+    return rc;
+}
+
+P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, double* cp, uint32_t* face,
+                      uint32_t* site, uint32_t* flags, p2m_counters* cnt) {
+    if (!e) { set_err("p2m_query: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (n && (!q || !dist || !cp || !face || !site)) { set_err("p2m_query: null buffer"); return P2M_ERR_INVALID; }
+    if (cnt) std::memset(cnt, 0, sizeof *cnt);
+    if (!n) return P2M_OK;
+    const int G = (int)e->slots.size();
+    std::vector<int> rcs(G, P2M_OK);
+    std::vector<p2m_counters> parts(G);
+    std::vector<std::string> errs(G);
+    auto work = [&](int g) {
+        const uint64_t b = n * (uint64_t)g / G, en = n * (uint64_t)(g + 1) / G, m = en - b;
+        parts[g] = p2m_counters{};
+        if (!m) return;
+        Slot& s = *e->slots[g];
+        std::lock_guard<std::mutex> lk(s.mu);
+        auto run = [&]() -> int {
+            CK(cudaSetDevice(s.dev));
+            // chunking: at least 1 Mi rows per chunk, about e->e2e_chunks chunks for large shards
+            const uint64_t nch = (uint64_t)std::max(1, e->e2e_chunks);
+            const uint64_t chunk = std::min<uint64_t>(m, std::max<uint64_t>(1ull << 20, (m + nch - 1) / nch));
+            int rc = ensure_ws(s, chunk);
+            if (rc != P2M_OK) return rc;
+            if (cnt) {
+                CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.pipe[0]));
+                CK(cudaEventRecord(s.agg_ready, s.pipe[0]));
+                for (int k = 1; k < Slot::kPipe; ++k) CK(cudaStreamWaitEvent(s.pipe[k], s.agg_ready, 0));
+            }
+            int c = 0;
+            for (uint64_t off = 0; off < m; off += chunk, ++c) {
+                const uint64_t len = std::min(chunk, m - off), r0 = b + off;
+                cudaStream_t st = s.pipe[c % Slot::kPipe];
+                Slot::Ws& w = s.ws[c % Slot::kPipe];  // reused only after this stream's previous D2H
+                CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, st));
+                p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
+                rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false);
+                if (rc != P2M_OK) return rc;
+                CK(cudaMemcpyAsync(dist + r0, w.dist, 8 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(cp + 3 * r0, w.cp, 24 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(face + r0, w.face, 4 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(site + r0, w.site, 4 * len, cudaMemcpyDeviceToHost, st));
+                if (flags) CK(cudaMemcpyAsync(flags + r0, w.flags, 4 * len, cudaMemcpyDeviceToHost, st));
+            }
+            for (auto& st : s.pipe) CK(cudaStreamSynchronize(st));
+            unsigned long long h[8] = {0};
+            if (cnt) CK(cudaMemcpy(h, s.agg, sizeof h, cudaMemcpyDeviceToHost));
+            parts[g].n_queries = m;
+            parts[g].candidates_visited = h[0];
+            parts[g].exact_evaluations = h[1];
+            parts[g].pruned = h[0] - h[1];
+            parts[g].kd_nodes_visited = h[2];
+            parts[g].filter_passes = h[4];
+            parts[g].warp_rare_iters = h[5];
+            parts[g].fallbacks = h[3];
+            return P2M_OK;
+        };
+        rcs[g] = run();
+        if (rcs[g] != P2M_OK) errs[g] = p2m_last_error();
+    };
+    if (G == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int g = 0; g < G; ++g) th.emplace_back(work, g);
+        for (auto& t : th) t.join();
+    }
+    for (int g = 0; g < G; ++g)
+        if (rcs[g] != P2M_OK) { set_err(errs[g]); return rcs[g]; }
+    if (cnt) {
+        for (auto& c : parts) {
+            cnt->n_queries += c.n_queries;
+            cnt->candidates_visited += c.candidates_visited;
+            cnt->exact_evaluations += c.exact_evaluations;
+            cnt->pruned += c.pruned;
+            cnt->kd_nodes_visited += c.kd_nodes_visited;
+            cnt->filter_passes += c.filter_passes;
+            cnt->warp_rare_iters += c.warp_rare_iters;
+            cnt->fallbacks += c.fallbacks;
+        }
+    }
+    return P2M_OK;
+}
+
+P2M_API int p2m_set_profiling(p2m_engine* e, int enable) {
+    if (!e) { set_err("engine not built"); return P2M_ERR_NOT_BUILT; }
+    e->profiling = enable != 0;
+    for (auto& s : e->slots) s->recorded = 0;
+    return P2M_OK;
+}
+
+// Mean per-call split over the calls recorded since profiling was (re)enabled; resets the ring.
+P2M_API int p2m_last_timings(p2m_engine* e, int slot, float* ms) {
+    if (!e || !ms || slot < 0 || slot >= (int)e->slots.size()) { set_err("p2m_last_timings: bad argument"); return P2M_ERR_INVALID; }
+    Slot& s = *e->slots[slot];
+    double acc[Slot::kEv] = {0};
+    CK(cudaSetDevice(s.dev));
+    for (int r = 0; r < s.recorded; ++r) {
+        cudaEvent_t* ev = &s.ev[Slot::kEv * r];
+        CK(cudaEventSynchronize(ev[Slot::kEv - 1]));
+        float m;
+        for (int k = 0; k + 1 < Slot::kEv; ++k) { CK(cudaEventElapsedTime(&m, ev[k], ev[k + 1])); acc[k] += m; }
+        CK(cudaEventElapsedTime(&m, ev[0], ev[Slot::kEv - 1])); acc[Slot::kEv - 1] += m;
+    }
+    for (int k = 0; k < Slot::kEv; ++k) ms[k] = s.recorded ? (float)(acc[k] / s.recorded) : 0.0f;
+    s.recorded = 0;
+    return P2M_OK;
+}
+
+P2M_API int p2m_set_scan_mode(p2m_engine* e, int mode) {
+    if (!e) { set_err("engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (mode != P2M_SCAN_GROUPED && mode != P2M_SCAN_FUSED) { set_err("p2m_set_scan_mode: unknown mode"); return P2M_ERR_INVALID; }
+    e->scan_mode = mode;
+    return P2M_OK;
+}
+
+// Count the kernels one p2m_query_device call launches by capturing it into a CUDA graph.
+P2M_API int p2m_kernels_per_query(p2m_engine* e, uint64_t n, int* launches) {
+    if (!e || !launches) { set_err("p2m_kernels_per_query: bad argument"); return P2M_ERR_INVALID; }
+    Slot& s = *e->slots[0];
+    CK(cudaSetDevice(s.dev));
+    if (!n) n = 1;
+    double *q = nullptr, *dist = nullptr, *cp = nullptr;
+    uint32_t *face = nullptr, *site = nullptr;
+    CK(cudaMalloc(&q, 24 * n)); CK(cudaMemset(q, 0, 24 * n));
+    CK(cudaMalloc(&dist, 8 * n)); CK(cudaMalloc(&cp, 24 * n)); CK(cudaMalloc(&face, 4 * n)); CK(cudaMalloc(&site, 4 * n));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    bool prof = e->profiling;
+    e->profiling = false;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    p2m::dev::Out o{dist, cp, face, site, nullptr, nullptr, nullptr};
+    int rc = run_pipeline(e, s, q, n, o, false, st, false, nullptr);
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(st, &g);
+    e->profiling = prof;
+    int k = 0;
+    if (rc == P2M_OK && g) {
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (auto& x : nodes) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(x, &t);
+            if (t == cudaGraphNodeTypeKernel) ++k;
+        }
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(st);
+    cudaFree(q); cudaFree(dist); cudaFree(cp); cudaFree(face); cudaFree(site);
+    if (rc != P2M_OK) return rc;
+    *launches = k;
+    return P2M_OK;
+}
