@@ -336,6 +336,9 @@ def main():
     e2e_value = n * world / shard.max_over_ranks(e2e_s, dist if world > 1 else None)
     # the e2e rows must equal the device-resident rows (same engine, same inputs)
     same = bool(torch.equal(o_dist, ddist.cpu()) and torch.equal(o_face, dface.cpu()))
+    if not same:
+        print("WARNING: p2m_query rows differ from p2m_query_device rows on the same inputs "
+              "(results must not depend on batching)", file=sys.stderr)
 
     if rank != 0:
         if world > 1:

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -192,6 +193,10 @@ struct Slot {
     // chunk, the kernels of another and the D2H copy of a third overlap
     static constexpr int kPipe = 4;
     cudaStream_t pipe[kPipe] = {};
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // one in-order copy stream per PCIe direction
+    static constexpr int kMaxChunks = 64;
+    std::vector<cudaEvent_t> cev;                // 3 per chunk: input landed, kernels done, output left
+    cudaEvent_t t0 = nullptr;                    // P2M_E2E_TRACE origin
     struct Ws {
         double *q = nullptr, *dist = nullptr, *cp = nullptr;
         uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
@@ -214,7 +219,7 @@ struct p2m_engine {
     uint64_t bytes = 0;
     bool profiling = false;
     int scan_mode = P2M_SCAN_GROUPED;
-    int e2e_chunks = 4;  // host-buffer path pipeline depth (P2M_E2E_CHUNKS overrides)
+    int e2e_chunks = 0;  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
     uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
@@ -238,6 +243,11 @@ void free_slot(Slot& s) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
     }
     for (auto& st : s.pipe) if (st) cudaStreamDestroy(st);
+    if (s.h2d) cudaStreamDestroy(s.h2d);
+    if (s.d2h) cudaStreamDestroy(s.d2h);
+    for (auto& e : s.cev) if (e) cudaEventDestroy(e);
+    s.cev.clear();
+    if (s.t0) cudaEventDestroy(s.t0);
     if (s.agg_ready) cudaEventDestroy(s.agg_ready);
     cudaFree(s.agg);
     for (auto& e : s.ev) if (e) cudaEventDestroy(e);
@@ -343,6 +353,13 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     for (auto& st : s.pipe) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking));
+    s.cev.assign(3 * Slot::kMaxChunks, nullptr);
+    // timing-capable only under P2M_E2E_TRACE (per-chunk timeline on stderr)
+    const bool trace = std::getenv("P2M_E2E_TRACE") != nullptr;
+    for (auto& e : s.cev) CK(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+    if (trace) CK(cudaEventCreate(&s.t0));
     CK(cudaEventCreateWithFlags(&s.agg_ready, cudaEventDisableTiming));
     CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
@@ -973,30 +990,79 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
         std::lock_guard<std::mutex> lk(s.mu);
         auto run = [&]() -> int {
             CK(cudaSetDevice(s.dev));
-            // chunking: at least 1 Mi rows per chunk, about e->e2e_chunks chunks for large shards
-            const uint64_t nch = (uint64_t)std::max(1, e->e2e_chunks);
-            const uint64_t chunk = std::min<uint64_t>(m, std::max<uint64_t>(1ull << 20, (m + nch - 1) / nch));
-            int rc = ensure_ws(s, chunk);
+            // Host-buffer pipeline.  PCIe, not the kernels, bounds this path (24 B in + 44 B out per
+            // row against ~1.6 G rows/s of kernels), so the schedule keeps both DMA directions busy:
+            //  * copies are issued in row order on ONE stream per direction, so each copy runs at full
+            //    link bandwidth instead of sharing it with the copies of later chunks;
+            //  * chunks grow geometrically from ~m/32 rows, so the first results start leaving the GPU
+            //    after a small H2D + kernel latency and the D2H stream then stays busy to the end;
+            //  * kernels of chunk c run on compute stream c % kPipe with staging set c % kPipe, after
+            //    its input landed and after the D2H of the chunk that used the set before it.
+            std::vector<uint64_t> len_of;
+            if (e->e2e_chunks > 0) {
+                const uint64_t k = (uint64_t)e->e2e_chunks;
+                const uint64_t c0 = std::max<uint64_t>(1ull << 20, (m + k - 1) / k);
+                for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
+            } else {
+                const uint64_t cmax = std::max<uint64_t>(1ull << 18, (m + 3) / 4);
+                uint64_t cur = std::min(cmax, std::max<uint64_t>(1ull << 18, m / 32));
+                for (uint64_t off = 0; off < m;) {
+                    const uint64_t l = std::min(cur, m - off);
+                    len_of.push_back(l);
+                    off += l;
+                    cur = std::min(cmax, 2 * cur);
+                }
+            }
+            if (len_of.size() > (size_t)Slot::kMaxChunks) {  // fold the tail into equal chunks
+                const uint64_t c0 = (m + Slot::kMaxChunks - 1) / Slot::kMaxChunks;
+                len_of.clear();
+                for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
+            }
+            uint64_t maxlen = 0;
+            for (uint64_t l : len_of) maxlen = std::max(maxlen, l);
+            int rc = ensure_ws(s, maxlen);
             if (rc != P2M_OK) return rc;
             if (cnt) {
                 CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.pipe[0]));
                 CK(cudaEventRecord(s.agg_ready, s.pipe[0]));
                 for (int k = 1; k < Slot::kPipe; ++k) CK(cudaStreamWaitEvent(s.pipe[k], s.agg_ready, 0));
             }
-            int c = 0;
-            for (uint64_t off = 0; off < m; off += chunk, ++c) {
-                const uint64_t len = std::min(chunk, m - off), r0 = b + off;
-                cudaStream_t st = s.pipe[c % Slot::kPipe];
-                Slot::Ws& w = s.ws[c % Slot::kPipe];  // reused only after this stream's previous D2H
-                CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, st));
+            if (s.t0) CK(cudaEventRecord(s.t0, s.h2d));
+            uint64_t off = 0;
+            for (size_t c = 0; c < len_of.size(); ++c) {
+                const uint64_t len = len_of[c], r0 = b + off;
+                off += len;
+                const int k = (int)(c % Slot::kPipe);
+                cudaStream_t st = s.pipe[k];
+                Slot::Ws& w = s.ws[k];
+                cudaEvent_t ev_in = s.cev[3 * c], ev_k = s.cev[3 * c + 1], ev_out = s.cev[3 * c + 2];
+                if (c >= (size_t)Slot::kPipe) CK(cudaStreamWaitEvent(s.h2d, s.cev[3 * (c - Slot::kPipe) + 1], 0));
+                CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, s.h2d));
+                CK(cudaEventRecord(ev_in, s.h2d));
+                CK(cudaStreamWaitEvent(st, ev_in, 0));
+                if (c >= (size_t)Slot::kPipe) CK(cudaStreamWaitEvent(st, s.cev[3 * (c - Slot::kPipe) + 2], 0));
                 p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
                 rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false);
                 if (rc != P2M_OK) return rc;
-                CK(cudaMemcpyAsync(dist + r0, w.dist, 8 * len, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(cp + 3 * r0, w.cp, 24 * len, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(face + r0, w.face, 4 * len, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(site + r0, w.site, 4 * len, cudaMemcpyDeviceToHost, st));
-                if (flags) CK(cudaMemcpyAsync(flags + r0, w.flags, 4 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaEventRecord(ev_k, st));
+                CK(cudaStreamWaitEvent(s.d2h, ev_k, 0));
+                CK(cudaMemcpyAsync(dist + r0, w.dist, 8 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaMemcpyAsync(cp + 3 * r0, w.cp, 24 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaMemcpyAsync(face + r0, w.face, 4 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaMemcpyAsync(site + r0, w.site, 4 * len, cudaMemcpyDeviceToHost, s.d2h));
+                if (flags) CK(cudaMemcpyAsync(flags + r0, w.flags, 4 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaEventRecord(ev_out, s.d2h));
+            }
+            CK(cudaStreamSynchronize(s.d2h));
+            if (s.t0) {
+                for (size_t c = 0; c < len_of.size(); ++c) {
+                    float a = 0, k = 0, o = 0;
+                    cudaEventElapsedTime(&a, s.t0, s.cev[3 * c]);
+                    cudaEventElapsedTime(&k, s.t0, s.cev[3 * c + 1]);
+                    cudaEventElapsedTime(&o, s.t0, s.cev[3 * c + 2]);
+                    std::fprintf(stderr, "e2e chunk %zu rows %llu: in %.3f  kernels %.3f  out %.3f ms\n", c,
+                                 (unsigned long long)len_of[c], a, k, o);
+                }
             }
             for (auto& st : s.pipe) CK(cudaStreamSynchronize(st));
             unsigned long long h[8] = {0};

@@ -17,6 +17,6 @@ for v in ${VARIANTS}; do
     env $envs P2M_LIB_DIR=$dir timeout 900 python bench.py --config $cfg $n --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ab_${name}_c$cfg.json 2> gpurun_out/ab_${name}_c$cfg.err
     python -c "
 import json; d=json.load(open('gpurun_out/ab_${name}_c$cfg.json')); s=d['config']['split_ms']; pq=d['config']['per_query']
-print('$name c$cfg', round(d['value']/1e6,1), 'Mq/s scan', round(s['scan'],3), 'E', round(pq['exact'],2), 'passes', round(pq.get('filter_passes',0),1))" 2>&1 | tail -1
+print('$name c$cfg', round(d['value']/1e6,1), 'Mq/s scan', round(s['scan'],3), 'E', round(pq['exact'],2), 'passes', round(pq.get('filter_passes',0),1), 'e2e', round(d['e2e']['value']/1e6,1), 'rows_equal', d['e2e']['rows_equal_device_path'])" 2>&1 | tail -1
   done
 done
