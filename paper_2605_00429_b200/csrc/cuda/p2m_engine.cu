@@ -428,6 +428,15 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
     size_t tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
     tb = std::max(tb, p2m::dev::tiles_tmp_bytes(n));
+    const uint64_t max_t = p2m::dev::max_tiles(n, E->n_sites);
+    // launch order of the scan tiles (P2M_TILE_ORDER): measured on c2, longest-first wins below a
+    // few million rows (the heaviest tiles otherwise start last and set the tail) and site order
+    // above (neighbouring tiles share lists in L2); -1 = choose by batch size
+    int order = s.params.tile_order;
+    if (order < 0) order = n < (4ull << 20) ? 1 : 0;
+    const bool lpt = order != 0;
+    if (grouped && lpt) tb = std::max(tb, p2m::dev::tile_order_tmp_bytes(max_t));
+    uint32_t* tord = nullptr;  // 4 x max_t: keys, sorted keys, tile ids, launch order
     CK(cudaMallocAsync(&keys, 4 * n, st));
     CK(cudaMallocAsync(&rows, 4 * n, st));
     CK(cudaMallocAsync(&keys2, 4 * n, st));
@@ -436,8 +445,9 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
     if (grouped) {
         CK(cudaMallocAsync(&flag, 4 * n, st));
         CK(cudaMallocAsync(&tix, 4 * n, st));
-        CK(cudaMallocAsync(&tiles, 4 * p2m::dev::max_tiles(n, E->n_sites), st));
+        CK(cudaMallocAsync(&tiles, 4 * max_t, st));
         CK(cudaMallocAsync(&meta, 16, st));
+        if (lpt) CK(cudaMallocAsync(&tord, 16 * max_t, st));
     }
     const bool prof = allow_prof && E->profiling && s.recorded < Slot::kRing;
     cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * s.recorded] : nullptr;
@@ -462,7 +472,28 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         // tiles over the site-sorted order (keys / rows2 are free again: hpos / run starts)
         CK(p2m::dev::launch_tiles(s.params, keys2, n, (uint32_t)E->n_sites, keys, rows2, flag, tix, tiles, meta, tmp, tb, st));
         if (prof) CK(cudaEventRecord(ev[4], st));
-        CK(p2m::dev::launch_scan_tiles(s.params, d_q, rows, keys2, tiles, meta, n, o, counters, st));
+        const char* trace_path = std::getenv("P2M_TILE_TRACE");
+        unsigned long long* trace = nullptr;
+        const uint64_t ntile_max = p2m::dev::max_tiles(n, E->n_sites);
+        Params prm = s.params;
+        prm.tile_order = order;
+        if (trace_path) {  // debug: per-tile timing dump (scripts/tile_trace.py)
+            CK(cudaMallocAsync(&trace, 32 * ntile_max, st));
+            CK(cudaMemsetAsync(trace, 0, 32 * ntile_max, st));
+            prm.tile_trace = trace;
+        }
+        if (tord)
+            CK(p2m::dev::launch_tile_order(prm, keys2, tiles, meta, max_t, tord, tord + max_t, tord + 2 * max_t,
+                                           tord + 3 * max_t, tmp, tb, st));
+        CK(p2m::dev::launch_scan_tiles(prm, d_q, rows, keys2, tiles, meta, tord ? tord + 3 * max_t : nullptr, n, o,
+                                       counters, st));
+        if (trace) {
+            std::vector<unsigned long long> h(4 * ntile_max);
+            CK(cudaMemcpyAsync(h.data(), trace, 32 * ntile_max, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (FILE* fp = std::fopen(trace_path, "wb")) { std::fwrite(h.data(), 8, h.size(), fp); std::fclose(fp); }
+            CK(cudaFreeAsync(trace, st));
+        }
         if (prof) CK(cudaEventRecord(ev[5], st));
     }
     CK(cudaFreeAsync(keys, st));
@@ -475,6 +506,7 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         CK(cudaFreeAsync(tix, st));
         CK(cudaFreeAsync(tiles, st));
         CK(cudaFreeAsync(meta, st));
+        if (tord) CK(cudaFreeAsync(tord, st));
     }
     return P2M_OK;
 }
@@ -884,10 +916,14 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
         s->params.grid_site = s->grid_site;
         s->params.nns = P2M_NNS_GRID;
+        s->params.tile_order = -1;
+        s->params.rpw_max = 8;
+        if (const char* v = std::getenv("P2M_RPW_MAX")) s->params.rpw_max = (uint32_t)std::atoi(v);
+        if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
         s->params.adj = s->adj;
     }
-    if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(0, std::atoi(v));
     {
         int rc = mark_heavy_sites(E.get(), d);
         if (rc != P2M_OK) return fail(rc);
@@ -1001,7 +1037,7 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             std::vector<uint64_t> len_of;
             if (e->e2e_chunks > 0) {
                 const uint64_t k = (uint64_t)e->e2e_chunks;
-                const uint64_t c0 = std::max<uint64_t>(1ull << 20, (m + k - 1) / k);
+                const uint64_t c0 = std::max<uint64_t>(1ull << 16, (m + k - 1) / k);
                 for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
             } else {
                 const uint64_t cmax = std::max<uint64_t>(1ull << 18, (m + 3) / 4);

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "p2m_device.cuh"
@@ -195,6 +196,168 @@ __device__ __forceinline__ float lb2_face(const float4* r, float qx, float qy, f
 constexpr int kChunk = 256;
 constexpr int kWinChunks = 256;                  // level-0 need bits are computed per window of chunks
 static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
+
+// ---- sparse tiles: one warp per row ---------------------------------------------------------
+// A tile with only a few rows cannot fill a CTA's lanes with rows, so each row gets a whole warp
+// that walks the row's list hierarchically with the lanes spread over LIST ENTRIES instead:
+// 32 chunk spheres per step (level 0, visited best-first), the 8 batch spheres of a chunk (level 1,
+// best-first), then 32 candidates of a batch at once (fp32 sphere test, tight fp32 lower bound, and
+// the exact fp64 kernel on every survivor in parallel), d_min updated after each batch by a warp
+// lexicographic (d^2, face id) reduction.  Same conservative tests as the tile path.
+__device__ __forceinline__ void warp_argmin(double& d, uint32_t& f) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
+        const uint32_t f2 = __shfl_xor_sync(0xffffffffu, f, o);
+        if (d2 < d || (d2 == d && f2 < f)) { d = d2; f = f2; }
+    }
+}
+
+template <bool kCounters>
+__device__ __noinline__ void scan_row_warp(const Params& p, const double* __restrict__ q_xyz, uint32_t row,
+                                           uint32_t s, const Out& o, int lane) {
+    const float K = 1.000001f;
+    const float delta = p.f32_delta;
+    const float finf = __int_as_float(0x7f800000);
+    const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+    const float qx = (float)q.x, qy = (float)q.y, qz = (float)q.z;
+    double best = __longlong_as_double(0x7ff0000000000000ll);
+    uint32_t bf = 0xffffffffu;
+    float DK = finf;                             // ((d_min up + delta) * K) up, warp-uniform
+    uint32_t exact = 0;
+    unsigned long long passes = 0;
+    auto set_dk = [&](double dm) { DK = __fmul_ru(__fadd_ru(__double2float_ru(dm), delta), K); };
+    if (!p.no_seed) {
+        const D4 rf = ldg4(p.site_ref + s);
+        if (rf.w != 0.0) set_dk(sqrt(vd2(q, V{rf.x, rf.y, rf.z})));
+    }
+    // conservative "may some member be within d_min" test against a group sphere
+    auto near = [&](float4 c, float& lbkey) {
+        const float dx = qx - c.x, dy = qy - c.y, dz = qz - c.z;
+        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+        lbkey = fmaxf(__fsqrt_rn(d2f) - c.w, 0.f);
+        const float th = __fadd_ru(c.w, DK);
+        return !(d2f > __fmul_ru(th, th));
+    };
+    const uint64_t beg = p.off[s], end = p.off[s + 1];
+    const uint64_t bo = p.boff[s], co = p.coff[s];
+    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+    if (!p.no_seed && !p.no_batch) {             // seed: min over chunk spheres of |q - C| + R
+        float ub = finf;
+        for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
+            if (c0 + lane < nch) {
+                const float4 c = p.csph[co + c0 + lane];
+                const float dx = qx - c.x, dy = qy - c.y, dz = qz - c.z;
+                const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                ub = fminf(ub, __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w));
+            }
+        }
+        ub = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(ub)));  // ub >= 0: uint order
+        const float cand = __fmul_ru(__fadd_ru(__fadd_ru(ub, delta), delta), K);
+        if (cand < DK) DK = cand;
+    }
+    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
+        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+        float ckey = finf;
+        bool cneed = false;
+        if (c0 + lane < nch) {
+            cs = p.csph[co + c0 + lane];
+            cneed = p.no_batch || near(cs, ckey);
+        }
+        uint32_t cm = __ballot_sync(0xffffffffu, cneed);
+        while (cm) {
+            // best-first: the needed chunk with the smallest lower bound (ties: lowest slot)
+            const uint32_t myk = ((cm >> lane) & 1u) ? __float_as_uint(ckey) : 0xffffffffu;
+            const uint32_t mk = __reduce_min_sync(0xffffffffu, myk);
+            const int k = __ffs(__ballot_sync(0xffffffffu, myk == mk && ((cm >> lane) & 1u))) - 1;
+            cm &= ~(1u << k);
+            float dummy;
+            const bool still = __shfl_sync(0xffffffffu, (int)(p.no_batch || (lane == k && near(cs, dummy))), k);
+            if (!still) continue;                // pruned by the d_min found meanwhile
+            const uint32_t cidx = c0 + k;
+            const uint64_t cb = beg + (uint64_t)cidx * kChunk;
+            const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
+            float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
+            float bkey = finf;
+            bool bneed = false;
+            if (lane < nb) {
+                bs = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + lane];
+                bneed = p.no_batch || near(bs, bkey);
+            }
+            uint32_t bm = __ballot_sync(0xffffffffu, bneed);
+            while (bm) {
+                const uint32_t myb = ((bm >> lane) & 1u) ? __float_as_uint(bkey) : 0xffffffffu;
+                const uint32_t mb = __reduce_min_sync(0xffffffffu, myb);
+                const int j = __ffs(__ballot_sync(0xffffffffu, myb == mb && ((bm >> lane) & 1u))) - 1;
+                bm &= ~(1u << j);
+                const bool bstill = __shfl_sync(0xffffffffu, (int)(p.no_batch || (lane == j && near(bs, dummy))), j);
+                if (!bstill) continue;
+                const uint64_t e = cb + 32ull * j + lane;
+                bool pass = false;
+                uint32_t f = 0;
+                if (e < end) {
+                    f = p.lfs[e];
+                    const float4 r = p.f32[f];
+                    const float dx = qx - r.x, dy = qy - r.y, dz = qz - r.z;
+                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                    const float th = __fadd_ru(r.w, DK);
+                    pass = !(d2f > __fmul_ru(th, th));
+                    if (pass) {
+                        const float thl = __fmul_ru(__fadd_ru(DK, p.lb_margin), 1.000001f);
+                        pass = !(lb2_face(p.lbr + 4 * (uint64_t)f, qx, qy, qz) > __fmul_ru(thl, thl));
+                    }
+                }
+                if (kCounters) passes += pass ? 1u : 0u;
+                double dd = __longlong_as_double(0x7ff0000000000000ll);
+                uint32_t ff = 0xffffffffu;
+                if (pass) {
+                    V a, b3, c3, pp3;
+                    load_tri(p.rec + 4 * (uint64_t)f, &a, &b3, &c3);
+                    dd = closest_tri(q, a, b3, c3, &pp3);
+                    ff = f;
+                }
+                exact += __popc(__ballot_sync(0xffffffffu, pass));
+                warp_argmin(dd, ff);
+                if (dd < best || (dd == best && ff < bf)) {
+                    best = dd;
+                    bf = ff;
+                    set_dk(sqrt(dd));
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+        V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+             __longlong_as_double(0x7ff8000000000000ll)};
+        if (bf != 0xffffffffu) {
+            V a, b3, c3;
+            load_tri(p.rec + 4 * (uint64_t)bf, &a, &b3, &c3);
+            closest_tri(q, a, b3, c3, &cp);
+        }
+        o.dist[row] = sqrt(best);
+        o.cp[3 * (uint64_t)row] = cp.x;
+        o.cp[3 * (uint64_t)row + 1] = cp.y;
+        o.cp[3 * (uint64_t)row + 2] = cp.z;
+        o.face[row] = bf;
+        if (kCounters) {
+            if (o.per_query) {
+                o.per_query[3 * (uint64_t)row] = end - beg;
+                o.per_query[3 * (uint64_t)row + 1] = exact;
+            }
+            if (o.agg) {
+                atomicAdd(o.agg + 0, (unsigned long long)(end - beg));
+                atomicAdd(o.agg + 1, (unsigned long long)exact);
+            }
+        }
+    }
+    if (kCounters && o.agg) {
+        unsigned long long v = passes;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) v += __shfl_down_sync(0xffffffffu, v, sh);
+        if (lane == 0) atomicAdd(o.agg + 4, v);
+    }
+}
+
 constexpr int kWarps = kTile / 32;
 
 #ifndef P2M_BATCH_ORDER
@@ -208,7 +371,8 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                                                          const uint32_t* __restrict__ rows,
                                                          const uint32_t* __restrict__ key,
                                                          const uint32_t* __restrict__ tiles,
-                                                         const uint32_t* __restrict__ meta, Out o) {
+                                                         const uint32_t* __restrict__ meta,
+                                                         const uint32_t* __restrict__ order, Out o) {
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
     __shared__ float4 s_lb[kChunk * 4];          // the chunk's fp32 lower-bound records (64 B each)
@@ -224,13 +388,23 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     __shared__ uint32_t s_rf[kTile];
     __shared__ uint32_t s_re[kTile];
     const uint32_t nt = meta[0];
-    const uint32_t b = blockIdx.x;
+    const uint32_t b = order ? order[blockIdx.x] : blockIdx.x;  // tiles launch longest-first
     if (b >= nt) return;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t start = tiles[b];
     const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
     const int m = (int)(stop - start);
     const uint32_t s = key[start];
+    const long long t_start = p.tile_trace ? clock64() : 0;
+    if (m <= (int)p.rpw_max) {                   // sparse tile: one warp per row
+        for (int j2 = w; j2 < m; j2 += kWarps) scan_row_warp<kCounters>(p, q_xyz, rows[start + j2], s, o, lane);
+        if (p.tile_trace && tid == 0) {
+            unsigned long long* t = p.tile_trace + 4 * (uint64_t)b;
+            t[0] = s; t[1] = (unsigned long long)m; t[2] = p.off[s + 1] - p.off[s];
+            t[3] = (unsigned long long)(clock64() - t_start) << 8;
+        }
+        return;
+    }
     const int G = (m + 31) >> 5;
     const int R = max(1, kWarps / G);
     const int r = w / G;                         // replica of this warp (uniform per warp)
@@ -404,12 +578,16 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                     const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
                     const uint64_t th = add2_up(pk2(B.z, B.w), DK);
                     const uint64_t t2 = mul2_up(th, th);
-                    float d0, d1, t0, t1;
-                    upk2(d2, d0, d1);
-                    upk2(t2, t0, t1);
-                    mask |= (uint32_t)(!(d0 > t0)) << (2 * pp);
-                    mask |= (uint32_t)(!(d1 > t1)) << (2 * pp + 1);
+                    // prune iff d2 > t2, i.e. iff fl(t2 - d2) is negative: IEEE subtraction keeps the
+                    // sign of the exact difference and gives +0 on equality (pass), and NaN from
+                    // inf - inf (padding against an unset d_min) has its sign bit clear (pass, masked
+                    // by valid) -- so one FADD2 and two funnel shifts collect the 32 prune bits
+                    float x0, x1;
+                    upk2(sub2(t2, d2), x0, x1);
+                    mask = __funnelshift_l(__float_as_uint(x0), mask, 1);
+                    mask = __funnelshift_l(__float_as_uint(x1), mask, 1);
                 }
+                mask = ~__brev(mask);  // bit k = candidate k passes
                 if (valid < 32) mask &= (1u << valid) - 1u;
             }
             uint32_t um = __reduce_or_sync(0xffffffffu, mask);
@@ -630,6 +808,13 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             }
         }
     }
+    if (p.tile_trace && tid == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* t = p.tile_trace + 4 * (uint64_t)b;
+        t[0] = s; t[1] = (unsigned long long)m; t[2] = p.off[s + 1] - p.off[s];
+        t[3] = (unsigned long long)(clock64() - t_start) << 8 | (smid & 0xff);
+    }
     const bool writer = active && r == 0;
     if (writer) {
         V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
@@ -721,13 +906,55 @@ cudaError_t launch_tiles(const Params& p, const uint32_t* key, uint64_t n, uint3
 
 uint64_t max_tiles(uint64_t n, uint64_t n_sites) { return std::min<uint64_t>(n, n_sites) + (n + 31) / 32 + 1; }
 
+// Longest-processing-time-first launch order of the tiles: a tile's time grows with its list
+// length and, more weakly, with its rows, and the heaviest tiles (long auxiliary lists) sit at the
+// END of the site-sorted order -- launched last, they would set a tail of up to ~2.5 ms on c2.
+__global__ void __launch_bounds__(256) k_tile_keys(Params p, const uint32_t* __restrict__ key,
+                                                   const uint32_t* __restrict__ tiles,
+                                                   const uint32_t* __restrict__ meta, uint32_t max_t,
+                                                   uint32_t* __restrict__ tkey, uint32_t* __restrict__ tidx) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= max_t) return;
+    const uint32_t nt = meta[0];
+    uint32_t k = 0;
+    if (t < nt) {
+        const uint32_t start = tiles[t];
+        const uint32_t stop = (t + 1 < nt) ? tiles[t + 1] : meta[1];
+        const uint32_t s = key[start];
+        const uint64_t len0 = p.off[s + 1] - p.off[s];
+        const uint64_t len = len0 < (1u << 20) ? len0 : (1u << 20);
+        if (p.tile_order == 1) k = (uint32_t)((len * (uint64_t)(stop - start + 16)) >> 4) + 1u;
+        else k = (uint32_t)(64 - __clzll((long long)len)) + 1u;  // bit length: coarse, keeps site order
+    }  // invalid tiles keep 0: launched last (and exit at once)
+    tkey[t] = k;
+    tidx[t] = t;
+}
+
+size_t tile_order_tmp_bytes(uint64_t max_t) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                              (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)max_t, 0, 32, 0);
+    return b;
+}
+
+cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32_t* tiles, const uint32_t* meta,
+                              uint64_t max_t, uint32_t* tkey, uint32_t* tkey2, uint32_t* tidx, uint32_t* order,
+                              void* tmp, size_t tmp_bytes, cudaStream_t s) {
+    if (!max_t) return cudaSuccess;
+    k_tile_keys<<<(unsigned)((max_t + 255) / 256), 256, 0, s>>>(p, key, tiles, meta, (uint32_t)max_t, tkey, tidx);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    size_t tb = tmp_bytes;
+    return cub::DeviceRadixSort::SortPairsDescending(tmp, tb, tkey, tkey2, tidx, order, (int64_t)max_t, 0, 32, s);
+}
+
 cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* rows, const uint32_t* key,
-                              const uint32_t* tiles, const uint32_t* meta, uint64_t n, const Out& o, bool counters,
-                              cudaStream_t s) {
+                              const uint32_t* tiles, const uint32_t* meta, const uint32_t* order, uint64_t n,
+                              const Out& o, bool counters, cudaStream_t s) {
     if (!n) return cudaSuccess;
     const unsigned g = (unsigned)max_tiles(n, p.n_nodes);
-    if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, o);
-    else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, o);
+    if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+    else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
     return cudaGetLastError();
 }
 

@@ -77,6 +77,9 @@ typedef struct p2m_engine_desc {
                                     auxiliary sites' projection proj(s, M) (REF/SPEC.md:238); ignored
                                     for mesh vertices (the vertex itself) and sentinels.  Seeds the
                                     grouped scan's d_min with the upper bound |q - ref| (result-neutral). */
+    const uint64_t *adj_offsets; /* optional (may be NULL): n_sites + 1, CSR of the Delaunay adjacency */
+    const uint32_t *adj_sites;   /* (sites whose Voronoi cells share a facet, symmetric, ascending);
+                                    enables the DelaunayWalk nearest-site strategy (REF/SPEC.md:476) */
 } p2m_engine_desc;
 
 /* Aggregate counters (REF/SPEC.md:468, 500, 511). */
@@ -146,6 +149,17 @@ int p2m_last_timings(p2m_engine *engine, int slot, float *ms);
 enum { P2M_SCAN_GROUPED = 0, P2M_SCAN_FUSED = 1 };
 int p2m_set_scan_mode(p2m_engine *engine, int mode);
 
+/* nearest_site strategy (REF/SPEC.md:473-481 NearestSiteIndex; all give the exact nearest site,
+ * ties -> lowest id, so results never depend on it -- "strategy neutrality", REF/SPEC.md:510):
+ *   P2M_NNS_GRID   (default) -- exact cell-locate grid over the Voronoi cell boxes, k-d tree
+ *                               outside the grid box / when the engine has no cell boxes
+ *   P2M_NNS_KDTREE           -- left-balanced k-d tree only
+ *   P2M_NNS_WALK             -- greedy descent on the Delaunay adjacency (REF/SPEC.md:476, 516),
+ *                               warm-started from a site listed in the query's grid cell (or site
+ *                               0); needs desc.adj_offsets, else P2M_ERR_INVALID */
+enum { P2M_NNS_GRID = 0, P2M_NNS_KDTREE = 1, P2M_NNS_WALK = 2 };
+int p2m_set_nns_strategy(p2m_engine *engine, int strategy);
+
 /* Number of kernels launched by one p2m_query_device call of n rows (for gpu_launches). */
 int p2m_kernels_per_query(p2m_engine *engine, uint64_t n, int *launches);
 
@@ -192,6 +206,42 @@ void p2m_build_config_default(p2m_build_config *cfg);
  * augment_sites -> cell corners -> build_all_tables -> per-face spheres (REF/SPEC.md:598-606). */
 int p2m_build(const double *vertices, uint64_t n_vertices, const uint32_t *faces, uint64_t n_faces,
               const p2m_build_config *cfg, p2m_host_engine **out);
+
+/* build_all_tables as a job (REF/SPEC.md:397-423, ball enumeration REF/SPEC.md:192-200): site s's
+ * list = every face f that meets one of its closed balls k -- a vertex of f within r2_k of c_k, or
+ * closest_on_triangle_sq(c_k, f) <= r2_k -- found by walking the builder's BVH with the box test
+ * box_sqdist(c_k) <= r2_k at every node from the root.  The set is fully determined by these
+ * arrays, so any executor that evaluates the same fp64 tests gives the same tables. */
+typedef struct p2m_table_job {
+    uint64_t n_sites;
+    const uint64_t *ball_off;   /* S+1 */
+    const double *balls;        /* 4 per ball: centre xyz, r^2 */
+    uint64_t n_faces;
+    const double *tri;          /* 9 per face */
+    uint64_t n_nodes;           /* BVH, depth-first: left child = node + 1 */
+    const double *node_box;     /* 6 per node: lo xyz, hi xyz */
+    const uint32_t *node_meta;  /* 3 per node: right child, first, count (count 0 = interior) */
+    const uint32_t *perm;       /* leaf face order */
+} p2m_table_job;
+/* Fills off[0..S] and *lists (allocated with malloc, freed by the builder); each list ascending. */
+typedef int (*p2m_table_fn)(void *ctx, const p2m_table_job *job, uint64_t *off, uint32_t **lists);
+/* p2m_build with the table phase delegated to fn (NULL = the builder's own host threads). */
+int p2m_build_with(const double *vertices, uint64_t n_vertices, const uint32_t *faces, uint64_t n_faces,
+                   const p2m_build_config *cfg, p2m_table_fn fn, void *ctx, p2m_host_engine **out);
+/* Delaunay adjacency of an arbitrary point set (no mesh): facet neighbours of the points' Voronoi
+ * cells bounded by the builder's sentinels, symmetric, ascending, sentinels dropped -- the
+ * DelaunayWalk graph (REF/SPEC.md:476) for queries inside 10x the points' AABB.  *off (n+1) and
+ * *adj are malloc'd; release with p2m_free. */
+int p2m_delaunay_adjacency(const double *xyz, uint64_t n, uint64_t **off, uint32_t **adj);
+
+/* (libp2m_cuda.so) p2m_build with the table job run on GPU `device`: one
+ * thread per ball walks a device copy of the same BVH, (site, face) hits are radix-sorted and
+ * deduplicated into the CSR.  Tables are bit-identical to p2m_build's; t_tables_s is the GPU
+ * phase including its copies. */
+int p2m_build_device(const double *vertices, uint64_t n_vertices, const uint32_t *faces,
+                     uint64_t n_faces, const p2m_build_config *cfg, int device, p2m_host_engine **out);
+/* The table job alone on GPU `device` (fn-compatible: ctx points to the int device id). */
+int p2m_table_job_device(void *ctx, const p2m_table_job *job, uint64_t *off, uint32_t **lists);
 void p2m_host_engine_destroy(p2m_host_engine *h);
 
 /* Pointers into the built engine (valid until destroy); feed straight into p2m_engine_create. */

@@ -92,9 +92,12 @@ struct Params {
                             // m_bc, m_ca, offset m_bc.(b-a) -- the tight lower bound sqrt(h^2+max(0,s_i)^2)
     float lb_margin;        // absolute fp32 error bound of that lower bound (64 * 2^-24 * M)
     const uint64_t* off;    // S+1
-    const uint64_t* boff;   // S+1: first batch sphere of each list (one per aligned 32 entries)
+    const uint64_t* boff;   // S+1: first batch sphere of each list (one per aligned 32 entries of lfs)
     const float4* bsph;     // batch spheres: centre rounded to nearest, radius (rounded up) * K
-    const uint32_t* lf;     // list entries
+    const uint32_t* lf;     // list entries, ascending (REF/SPEC.md:392; the fused sequential path)
+    const uint32_t* lfs;    // the same lists in spatial (Morton) order (the grouped scan)
+    const uint64_t* coff;   // S+1: first chunk sphere of each list (one per aligned 256 entries of lfs)
+    const float4* csph;     // chunk spheres, same conservative form as bsph
     const D4* bvh;          // 2 per node
     const uint32_t* bvh_perm;  // leaf face ids
     uint32_t n_faces;
@@ -112,6 +115,9 @@ struct Params {
     int no_batch;           // 1: no level-1 batch-sphere pruning (P2M_NO_BATCH)
     const uint32_t* grid_off;
     const uint32_t* grid_site;
+    int nns;                // P2M_NNS_* strategy of nearest_site
+    const uint64_t* adj_off;  // Delaunay adjacency CSR (nullptr: no DelaunayWalk)
+    const uint32_t* adj;
     double grid_lo[3], grid_inv[3];
     uint32_t grid_res[3];
 };

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -47,6 +48,26 @@ void set_err(const std::string& s) { p2m_set_last_error_internal(s.c_str()); }
     } while (0)
 
 // ---- host-side packing --------------------------------------------------------------------
+
+constexpr uint64_t kListChunk = 256;  // = k_scan_tiles' chunk (p2m_grouped.cu kChunk)
+
+// fn(s0, s1) over contiguous site ranges on all hardware threads
+template <class Fn>
+void parallel_sites(uint64_t S, Fn&& fn) {
+    const unsigned T = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    const uint64_t step = std::max<uint64_t>(1024, (S + T * 8 - 1) / (T * 8));
+    std::atomic<uint64_t> next{0};
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t)
+        th.emplace_back([&] {
+            for (;;) {
+                const uint64_t a = next.fetch_add(step);
+                if (a >= S) break;
+                fn(a, std::min(S, a + step));
+            }
+        });
+    for (auto& x : th) x.join();
+}
 
 uint64_t lb_left_size(uint64_t n) {
     if (n <= 1) return 0;
@@ -154,20 +175,28 @@ struct Slot {
     D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
     float4* f32 = nullptr;
     float4* bsph = nullptr;
+    float4* csph = nullptr;
     float4* lbr = nullptr;
     uint64_t* boff = nullptr;
+    uint64_t* coff = nullptr;
     uint64_t* off = nullptr;
-    uint32_t *lf = nullptr, *bvh_perm = nullptr;
+    uint32_t *lf = nullptr, *lfs = nullptr, *bvh_perm = nullptr;
     uint8_t* heavy = nullptr;
     D4* site_pos = nullptr;
     D4* site_ref = nullptr;
     uint32_t *grid_off = nullptr, *grid_site = nullptr;
+    uint64_t* adj_off = nullptr;
+    uint32_t* adj = nullptr;
     Params params{};
     std::mutex mu;
     // host-API path: kPipe streams, each with a chunk-sized staging set, so the H2D copy of one
     // chunk, the kernels of another and the D2H copy of a third overlap
     static constexpr int kPipe = 4;
     cudaStream_t pipe[kPipe] = {};
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // one in-order copy stream per PCIe direction
+    static constexpr int kMaxChunks = 64;
+    std::vector<cudaEvent_t> cev;                // 3 per chunk: input landed, kernels done, output left
+    cudaEvent_t t0 = nullptr;                    // P2M_E2E_TRACE origin
     struct Ws {
         double *q = nullptr, *dist = nullptr, *cp = nullptr;
         uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
@@ -190,10 +219,13 @@ struct p2m_engine {
     uint64_t bytes = 0;
     bool profiling = false;
     int scan_mode = P2M_SCAN_GROUPED;
-    int e2e_chunks = 4;  // host-buffer path pipeline depth (P2M_E2E_CHUNKS overrides)
+    int e2e_chunks = 0;  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
     uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
+    uint64_t n_chunks = 0;                    // 256-entry list chunks (chunk spheres)
+    uint64_t n_adj = 0;                       // Delaunay adjacency entries (0 = no walk strategy)
+    bool has_adj = false;
 };
 
 namespace {
@@ -205,10 +237,17 @@ void free_slot(Slot& s) {
     cudaFree(s.site_pos); cudaFree(s.site_ref); cudaFree(s.grid_off); cudaFree(s.grid_site);
     cudaFree(s.f32);
     cudaFree(s.bsph); cudaFree(s.boff); cudaFree(s.lbr);
+    cudaFree(s.csph); cudaFree(s.coff); cudaFree(s.lfs);
+    cudaFree(s.adj_off); cudaFree(s.adj);
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
     }
     for (auto& st : s.pipe) if (st) cudaStreamDestroy(st);
+    if (s.h2d) cudaStreamDestroy(s.h2d);
+    if (s.d2h) cudaStreamDestroy(s.d2h);
+    for (auto& e : s.cev) if (e) cudaEventDestroy(e);
+    s.cev.clear();
+    if (s.t0) cudaEventDestroy(s.t0);
     if (s.agg_ready) cudaEventDestroy(s.agg_ready);
     cudaFree(s.agg);
     for (auto& e : s.ev) if (e) cudaEventDestroy(e);
@@ -314,6 +353,13 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     for (auto& st : s.pipe) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking));
+    s.cev.assign(3 * Slot::kMaxChunks, nullptr);
+    // timing-capable only under P2M_E2E_TRACE (per-chunk timeline on stderr)
+    const bool trace = std::getenv("P2M_E2E_TRACE") != nullptr;
+    for (auto& e : s.cev) CK(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+    if (trace) CK(cudaEventCreate(&s.t0));
     CK(cudaEventCreateWithFlags(&s.agg_ready, cudaEventDisableTiming));
     CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
@@ -323,12 +369,19 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.boff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
+    CK(cudaMalloc(&s.lfs, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
+    CK(cudaMalloc(&s.csph, sizeof(float4) * std::max<uint64_t>(1, E.n_chunks)));
+    CK(cudaMalloc(&s.coff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
     CK(cudaMalloc(&s.bvh_perm, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.agg, sizeof(unsigned long long) * 8));
     CK(cudaMalloc(&s.heavy, std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.site_pos, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.site_ref, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
+    if (E.has_adj) {
+        CK(cudaMalloc(&s.adj_off, 8 * (E.n_sites + 1)));
+        CK(cudaMalloc(&s.adj, 4 * std::max<uint64_t>(1, E.n_adj)));
+    }
     if (E.grid_cells) {
         CK(cudaMalloc(&s.grid_off, 4 * (E.grid_cells + 1)));
         CK(cudaMalloc(&s.grid_site, 4 * std::max<uint64_t>(1, E.grid_pairs)));
@@ -497,6 +550,15 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
 
     auto E = std::make_unique<p2m_engine>();
     E->n_sites = S; E->n_faces = F; E->n_entries = L;
+    if (d->adj_offsets && d->adj_sites) {
+        if (d->adj_offsets[0] != 0) { set_err("p2m_engine_create: adjacency offsets must start at 0"); return P2M_ERR_INVALID; }
+        for (uint64_t s = 0; s < S; ++s)
+            if (d->adj_offsets[s] > d->adj_offsets[s + 1]) { set_err("p2m_engine_create: adjacency offsets not monotone"); return P2M_ERR_INVALID; }
+        for (uint64_t k = 0; k < d->adj_offsets[S]; ++k)
+            if (d->adj_sites[k] >= S) { set_err("p2m_engine_create: adjacency site id out of range"); return P2M_ERR_INVALID; }
+        E->has_adj = true;
+        E->n_adj = d->adj_offsets[S];
+    }
 
     // ---- pack ----
     std::vector<uint32_t> node_site;
@@ -544,41 +606,95 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
         f32[f] = make_float4((float)sp[0], (float)sp[1], (float)sp[2], rk);
     }
-    // level-1 pruning spheres: one per aligned 32-entry batch of every list.  Centre = centre of the
-    // members' sphere boxes; radius = max |c_i - C| + r_i, then made conservative for the fp32
-    // kernel test (centre rounded to nearest, radius grown by the centre's rounding and rounded up,
-    // times K rounded up -- the same form as the per-face records)
-    std::vector<uint64_t> boff(S + 1, 0);
-    for (uint64_t s = 0; s < S; ++s) boff[s + 1] = boff[s] + (d->list_offsets[s + 1] - d->list_offsets[s] + 31) / 32;
-    E->n_batches = boff[S];
-    std::vector<float4> bsph(std::max<uint64_t>(1, E->n_batches));
-    for (uint64_t s = 0; s < S; ++s) {
-        const uint64_t b0 = d->list_offsets[s], b1 = d->list_offsets[s + 1];
-        for (uint64_t j = b0, bi = boff[s]; j < b1; j += 32, ++bi) {
-            const uint64_t je = std::min(b1, j + 32);
-            double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-            for (uint64_t t = j; t < je; ++t) {
-                const double* sp = d->face_sphere + 4 * (uint64_t)d->list_faces[t];
-                for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], sp[k] - sp[3]); hi[k] = std::max(hi[k], sp[k] + sp[3]); }
+    // Spatial list order for the grouped scan (lfs): the (d^2, face id) argmin does not depend on
+    // the order a list is scanned in, so each list is re-sorted by the Morton code of its faces'
+    // sphere centres (ties by id) -- its 32-entry batches and 256-entry chunks then enclose compact
+    // surface patches and their spheres prune whole.  lf keeps the ascending order of
+    // REF/SPEC.md:392 for the sequential fused path (oracle-identical counters).
+    std::vector<uint32_t> lfs(std::max<uint64_t>(1, L));
+    {
+        double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (uint64_t f = 0; f < F; ++f)
+            for (int k = 0; k < 3; ++k) {
+                clo[k] = std::min(clo[k], d->face_sphere[4 * f + k]);
+                chi[k] = std::max(chi[k], d->face_sphere[4 * f + k]);
             }
-            double C[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
-            float cf[3] = {(float)C[0], (float)C[1], (float)C[2]};
-            double R = 0.0;
-            for (uint64_t t = j; t < je; ++t) {
-                const double* sp = d->face_sphere + 4 * (uint64_t)d->list_faces[t];
-                double dd = 0.0;
-                for (int k = 0; k < 3; ++k) dd += (sp[k] - (double)cf[k]) * (sp[k] - (double)cf[k]);
-                R = std::max(R, std::sqrt(dd) + sp[3]);
+        std::vector<uint64_t> fkey(F);
+        auto spread = [](uint64_t x) {  // 21 bits -> every third bit
+            x &= 0x1fffff;
+            x = (x | x << 32) & 0x1f00000000ffffull;
+            x = (x | x << 16) & 0x1f0000ff0000ffull;
+            x = (x | x << 8) & 0x100f00f00f00f00full;
+            x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+            x = (x | x << 2) & 0x1249249249249249ull;
+            return x;
+        };
+        for (uint64_t f = 0; f < F; ++f) {
+            uint64_t key = 0;
+            for (int k = 0; k < 3; ++k) {
+                const double ext = chi[k] - clo[k];
+                const double t = ext > 0 ? (d->face_sphere[4 * f + k] - clo[k]) / ext : 0.0;
+                key |= spread((uint64_t)std::min(2097151.0, std::max(0.0, t * 2097152.0))) << k;
             }
-            R = R * (1.0 + 1e-12) + 1e-300;
-            float rf = (float)R;
-            if ((double)rf < R) rf = std::nextafter(rf, INFINITY);
-            const double prod = (double)rf * (double)1.000001f;
-            float rk = (float)prod;
-            if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
-            bsph[bi] = make_float4(cf[0], cf[1], cf[2], rk);
+            fkey[f] = key;
         }
+        const bool spatial = std::getenv("P2M_NO_SPATIAL") == nullptr;
+        parallel_sites(S, [&](uint64_t s0, uint64_t s1) {
+            std::vector<std::pair<uint64_t, uint32_t>> tmp;
+            for (uint64_t s = s0; s < s1; ++s) {
+                const uint64_t b0 = d->list_offsets[s], b1 = d->list_offsets[s + 1];
+                tmp.clear();
+                for (uint64_t j = b0; j < b1; ++j) tmp.push_back({spatial ? fkey[d->list_faces[j]] : 0ull, d->list_faces[j]});
+                std::sort(tmp.begin(), tmp.end());
+                for (uint64_t j = b0; j < b1; ++j) lfs[j] = tmp[j - b0].second;
+            }
+        });
     }
+    // level-1 / level-0 pruning spheres over lfs: one per aligned 32-entry batch and one per aligned
+    // 256-entry chunk of every list.  Centre = centre of the members' sphere boxes; radius =
+    // max |c_i - C| + r_i, then made conservative for the fp32 kernel test (centre rounded to
+    // nearest, radius grown by the centre's rounding and rounded up, times K rounded up -- the same
+    // form as the per-face records)
+    auto group_sphere = [&](uint64_t j, uint64_t je) {
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (uint64_t t = j; t < je; ++t) {
+            const double* sp = d->face_sphere + 4 * (uint64_t)lfs[t];
+            for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], sp[k] - sp[3]); hi[k] = std::max(hi[k], sp[k] + sp[3]); }
+        }
+        double C[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+        float cf[3] = {(float)C[0], (float)C[1], (float)C[2]};
+        double R = 0.0;
+        for (uint64_t t = j; t < je; ++t) {
+            const double* sp = d->face_sphere + 4 * (uint64_t)lfs[t];
+            double dd = 0.0;
+            for (int k = 0; k < 3; ++k) dd += (sp[k] - (double)cf[k]) * (sp[k] - (double)cf[k]);
+            R = std::max(R, std::sqrt(dd) + sp[3]);
+        }
+        R = R * (1.0 + 1e-12) + 1e-300;
+        float rf = (float)R;
+        if ((double)rf < R) rf = std::nextafter(rf, INFINITY);
+        const double prod = (double)rf * (double)1.000001f;
+        float rk = (float)prod;
+        if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
+        return make_float4(cf[0], cf[1], cf[2], rk);
+    };
+    std::vector<uint64_t> boff(S + 1, 0), coff(S + 1, 0);
+    for (uint64_t s = 0; s < S; ++s) {
+        const uint64_t len = d->list_offsets[s + 1] - d->list_offsets[s];
+        boff[s + 1] = boff[s] + (len + 31) / 32;
+        coff[s + 1] = coff[s] + (len + kListChunk - 1) / kListChunk;
+    }
+    E->n_batches = boff[S];
+    E->n_chunks = coff[S];
+    std::vector<float4> bsph(std::max<uint64_t>(1, E->n_batches)), csph(std::max<uint64_t>(1, E->n_chunks));
+    parallel_sites(S, [&](uint64_t s0, uint64_t s1) {
+        for (uint64_t s = s0; s < s1; ++s) {
+            const uint64_t b0 = d->list_offsets[s], b1 = d->list_offsets[s + 1];
+            for (uint64_t j = b0, bi = boff[s]; j < b1; j += 32, ++bi) bsph[bi] = group_sphere(j, std::min(b1, j + 32));
+            for (uint64_t j = b0, ci = coff[s]; j < b1; j += kListChunk, ++ci)
+                csph[ci] = group_sphere(j, std::min(b1, j + kListChunk));
+        }
+    });
     // tight fp32 lower-bound records (k_scan_tiles rare path): d(q,T)^2 >= h^2 + max(0, s_i)^2 with
     // h = n.(q-a) and s_i the signed in-plane distances to the three edge lines (outward positive)
     std::vector<float4> lbr(4 * std::max<uint64_t>(1, F));
@@ -704,18 +820,24 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             cudaMemcpy(s0.lbr, lbr.data(), sizeof(float4) * lbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
+            (L && cudaMemcpy(s0.lfs, lfs.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
+            cudaMemcpy(s0.csph, csph.data(), sizeof(float4) * csph.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(s0.coff, coff.data(), 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.site_pos, site_pos.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
             cudaMemcpy(s0.site_ref, site_ref.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
+            (E->has_adj && cudaMemcpy(s0.adj_off, d->adj_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
+            (E->n_adj && cudaMemcpy(s0.adj, d->adj_sites, 4 * E->n_adj, cudaMemcpyHostToDevice) != cudaSuccess) ||
             (E->grid_cells && cudaMemcpy(s0.grid_off, grid.off.data(), 4 * (E->grid_cells + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
             (E->grid_pairs && cudaMemcpy(s0.grid_site, grid.site.data(), 4 * E->grid_pairs, cudaMemcpyHostToDevice) != cudaSuccess)) {
             set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
             return fail(P2M_ERR_CUDA);
         }
     }
-    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (5 * F + E->n_batches) + 8 * (S + 1) + 8 * (S + 1) + 4 * (L + F) + S +
-               (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0);
+    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (5 * F + E->n_batches + E->n_chunks) +
+               3 * 8 * (S + 1) + 4 * (2 * L + F) + S +
+               (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0) + (E->has_adj ? 8 * (S + 1) + 4 * E->n_adj : 0);
     auto t0 = std::chrono::steady_clock::now();
     for (size_t k = 1; k < E->slots.size(); ++k) {
         Slot& s = *E->slots[k];
@@ -734,10 +856,13 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             {s.bsph, s0.bsph, sizeof(float4) * std::max<uint64_t>(1, E->n_batches)}, {s.boff, s0.boff, 8 * (S + 1)},
             {s.lbr, s0.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, F)},
             {s.off, s0.off, 8 * (S + 1)},
-            {s.lf, s0.lf, 4 * L}, {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
+            {s.lf, s0.lf, 4 * L}, {s.lfs, s0.lfs, 4 * L},
+            {s.csph, s0.csph, sizeof(float4) * std::max<uint64_t>(1, E->n_chunks)}, {s.coff, s0.coff, 8 * (S + 1)},
+            {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
             {s.site_pos, s0.site_pos, sizeof(D4) * S}, {s.site_ref, s0.site_ref, sizeof(D4) * S},
             {s.grid_off, s0.grid_off, E->grid_cells ? 4 * (E->grid_cells + 1) : 0},
-            {s.grid_site, s0.grid_site, 4 * E->grid_pairs}};
+            {s.grid_site, s0.grid_site, 4 * E->grid_pairs},
+            {s.adj_off, s0.adj_off, E->has_adj ? 8 * (S + 1) : 0}, {s.adj, s0.adj, 4 * E->n_adj}};
         for (auto& c : cp)
             if (c.n && cudaMemcpyPeerAsync(c.dst, s.dev, c.src, s0.dev, c.n, s.stream) != cudaSuccess) {
                 set_err("p2m_engine_create: peer copy failed");
@@ -752,11 +877,15 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     for (auto& s : E->slots) {
         s->params = P;
         s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.lbr = s->lbr; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.lfs = s->lfs; s->params.csph = s->csph; s->params.coff = s->coff;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
         s->params.site_pos = s->site_pos;
         s->params.site_ref = s->site_ref;
         s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
         s->params.grid_site = s->grid_site;
+        s->params.nns = P2M_NNS_GRID;
+        s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
+        s->params.adj = s->adj;
     }
     if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(1, std::atoi(v));
     {
@@ -861,30 +990,79 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
         std::lock_guard<std::mutex> lk(s.mu);
         auto run = [&]() -> int {
             CK(cudaSetDevice(s.dev));
-            // chunking: at least 1 Mi rows per chunk, about e->e2e_chunks chunks for large shards
-            const uint64_t nch = (uint64_t)std::max(1, e->e2e_chunks);
-            const uint64_t chunk = std::min<uint64_t>(m, std::max<uint64_t>(1ull << 20, (m + nch - 1) / nch));
-            int rc = ensure_ws(s, chunk);
+            // Host-buffer pipeline.  PCIe, not the kernels, bounds this path (24 B in + 44 B out per
+            // row against ~1.6 G rows/s of kernels), so the schedule keeps both DMA directions busy:
+            //  * copies are issued in row order on ONE stream per direction, so each copy runs at full
+            //    link bandwidth instead of sharing it with the copies of later chunks;
+            //  * chunks grow geometrically from ~m/32 rows, so the first results start leaving the GPU
+            //    after a small H2D + kernel latency and the D2H stream then stays busy to the end;
+            //  * kernels of chunk c run on compute stream c % kPipe with staging set c % kPipe, after
+            //    its input landed and after the D2H of the chunk that used the set before it.
+            std::vector<uint64_t> len_of;
+            if (e->e2e_chunks > 0) {
+                const uint64_t k = (uint64_t)e->e2e_chunks;
+                const uint64_t c0 = std::max<uint64_t>(1ull << 20, (m + k - 1) / k);
+                for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
+            } else {
+                const uint64_t cmax = std::max<uint64_t>(1ull << 18, (m + 3) / 4);
+                uint64_t cur = std::min(cmax, std::max<uint64_t>(1ull << 18, m / 32));
+                for (uint64_t off = 0; off < m;) {
+                    const uint64_t l = std::min(cur, m - off);
+                    len_of.push_back(l);
+                    off += l;
+                    cur = std::min(cmax, 2 * cur);
+                }
+            }
+            if (len_of.size() > (size_t)Slot::kMaxChunks) {  // fold the tail into equal chunks
+                const uint64_t c0 = (m + Slot::kMaxChunks - 1) / Slot::kMaxChunks;
+                len_of.clear();
+                for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
+            }
+            uint64_t maxlen = 0;
+            for (uint64_t l : len_of) maxlen = std::max(maxlen, l);
+            int rc = ensure_ws(s, maxlen);
             if (rc != P2M_OK) return rc;
             if (cnt) {
                 CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.pipe[0]));
                 CK(cudaEventRecord(s.agg_ready, s.pipe[0]));
                 for (int k = 1; k < Slot::kPipe; ++k) CK(cudaStreamWaitEvent(s.pipe[k], s.agg_ready, 0));
             }
-            int c = 0;
-            for (uint64_t off = 0; off < m; off += chunk, ++c) {
-                const uint64_t len = std::min(chunk, m - off), r0 = b + off;
-                cudaStream_t st = s.pipe[c % Slot::kPipe];
-                Slot::Ws& w = s.ws[c % Slot::kPipe];  // reused only after this stream's previous D2H
-                CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, st));
+            if (s.t0) CK(cudaEventRecord(s.t0, s.h2d));
+            uint64_t off = 0;
+            for (size_t c = 0; c < len_of.size(); ++c) {
+                const uint64_t len = len_of[c], r0 = b + off;
+                off += len;
+                const int k = (int)(c % Slot::kPipe);
+                cudaStream_t st = s.pipe[k];
+                Slot::Ws& w = s.ws[k];
+                cudaEvent_t ev_in = s.cev[3 * c], ev_k = s.cev[3 * c + 1], ev_out = s.cev[3 * c + 2];
+                if (c >= (size_t)Slot::kPipe) CK(cudaStreamWaitEvent(s.h2d, s.cev[3 * (c - Slot::kPipe) + 1], 0));
+                CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, s.h2d));
+                CK(cudaEventRecord(ev_in, s.h2d));
+                CK(cudaStreamWaitEvent(st, ev_in, 0));
+                if (c >= (size_t)Slot::kPipe) CK(cudaStreamWaitEvent(st, s.cev[3 * (c - Slot::kPipe) + 2], 0));
                 p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
                 rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false);
                 if (rc != P2M_OK) return rc;
-                CK(cudaMemcpyAsync(dist + r0, w.dist, 8 * len, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(cp + 3 * r0, w.cp, 24 * len, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(face + r0, w.face, 4 * len, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(site + r0, w.site, 4 * len, cudaMemcpyDeviceToHost, st));
-                if (flags) CK(cudaMemcpyAsync(flags + r0, w.flags, 4 * len, cudaMemcpyDeviceToHost, st));
+                CK(cudaEventRecord(ev_k, st));
+                CK(cudaStreamWaitEvent(s.d2h, ev_k, 0));
+                CK(cudaMemcpyAsync(dist + r0, w.dist, 8 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaMemcpyAsync(cp + 3 * r0, w.cp, 24 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaMemcpyAsync(face + r0, w.face, 4 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaMemcpyAsync(site + r0, w.site, 4 * len, cudaMemcpyDeviceToHost, s.d2h));
+                if (flags) CK(cudaMemcpyAsync(flags + r0, w.flags, 4 * len, cudaMemcpyDeviceToHost, s.d2h));
+                CK(cudaEventRecord(ev_out, s.d2h));
+            }
+            CK(cudaStreamSynchronize(s.d2h));
+            if (s.t0) {
+                for (size_t c = 0; c < len_of.size(); ++c) {
+                    float a = 0, k = 0, o = 0;
+                    cudaEventElapsedTime(&a, s.t0, s.cev[3 * c]);
+                    cudaEventElapsedTime(&k, s.t0, s.cev[3 * c + 1]);
+                    cudaEventElapsedTime(&o, s.t0, s.cev[3 * c + 2]);
+                    std::fprintf(stderr, "e2e chunk %zu rows %llu: in %.3f  kernels %.3f  out %.3f ms\n", c,
+                                 (unsigned long long)len_of[c], a, k, o);
+                }
             }
             for (auto& st : s.pipe) CK(cudaStreamSynchronize(st));
             unsigned long long h[8] = {0};
@@ -955,6 +1133,23 @@ P2M_API int p2m_set_scan_mode(p2m_engine* e, int mode) {
     if (!e) { set_err("engine not built"); return P2M_ERR_NOT_BUILT; }
     if (mode != P2M_SCAN_GROUPED && mode != P2M_SCAN_FUSED) { set_err("p2m_set_scan_mode: unknown mode"); return P2M_ERR_INVALID; }
     e->scan_mode = mode;
+    return P2M_OK;
+}
+
+P2M_API int p2m_set_nns_strategy(p2m_engine* e, int strategy) {
+    if (!e) { set_err("engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (strategy != P2M_NNS_GRID && strategy != P2M_NNS_KDTREE && strategy != P2M_NNS_WALK) {
+        set_err("p2m_set_nns_strategy: unknown strategy");
+        return P2M_ERR_INVALID;
+    }
+    if (strategy == P2M_NNS_WALK && !e->has_adj) {
+        set_err("p2m_set_nns_strategy: DelaunayWalk needs the engine's Delaunay adjacency (desc.adj_offsets)");
+        return P2M_ERR_INVALID;
+    }
+    for (auto& s : e->slots) {
+        std::lock_guard<std::mutex> lk(s->mu);
+        s->params.nns = strategy;
+    }
     return P2M_OK;
 }
 

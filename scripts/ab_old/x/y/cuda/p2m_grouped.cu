@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_descend(Params p, const double* __restr
     if (i < n) {
         const uint32_t row = rows[i];
         const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
-        const NN nn = nearest_site_cl(p, q);
+        const NN nn = nearest_site_any(p, q);
         visited = nn.visited;
         const bool in_d = q.x >= p.dmin[0] && q.x <= p.dmax[0] && q.y >= p.dmin[1] && q.y <= p.dmax[1] &&
                           q.z >= p.dmin[2] && q.z <= p.dmax[2];
@@ -193,10 +193,18 @@ __device__ __forceinline__ float lb2_face(const float4* r, float qx, float qy, f
 // sequential oracle would (so with R = 1 the counters match the oracle too).  Replicas are merged by
 // the lexicographic min of (d^2, face id), the sequential argmin.
 constexpr int kChunk = 256;
+constexpr int kWinChunks = 256;                  // level-0 need bits are computed per window of chunks
+static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 constexpr int kWarps = kTile / 32;
 
+#ifndef P2M_BATCH_ORDER
+#define P2M_BATCH_ORDER 1   // block path: visit a chunk's batches best-first for the tile's first row
+#endif
+#ifndef P2M_SCAN_MINB
+#define P2M_SCAN_MINB 4  // resident CTAs per SM the register budget is sized for (measured: 4 > 3 > 2)
+#endif
 template <bool kCounters>
-__global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
+__global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
                                                          const uint32_t* __restrict__ rows,
                                                          const uint32_t* __restrict__ key,
                                                          const uint32_t* __restrict__ tiles,
@@ -206,6 +214,12 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     __shared__ float4 s_lb[kChunk * 4];          // the chunk's fp32 lower-bound records (64 B each)
     __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
     __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
+    __shared__ uint32_t s_cw[kWinChunks / 32];   // chunks of the current window some row must scan
+    __shared__ uint32_t s_oidx[kWinChunks];      // ... in visiting order
+    __shared__ uint32_t s_okey[kWinChunks];
+    __shared__ float4 s_qrep;                    // the tile's first row (fp32), for the visiting order
+    __shared__ uint32_t s_next;                  // small tiles: next batch of the window to scan
+    __shared__ uint8_t s_bord[kChunk / 32];      // block path: visiting order of the chunk's batches
     __shared__ double s_rd[kTile];
     __shared__ uint32_t s_rf[kTile];
     __shared__ uint32_t s_re[kTile];
@@ -231,6 +245,7 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
         q = V{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
         const float fx = (float)q.x, fy = (float)q.y, fz = (float)q.z;
         QX = pk2(fx, fx); QY = pk2(fy, fy); QZ = pk2(fz, fz);
+        if (tid == 0) s_qrep = make_float4(fx, fy, fz, 0.f);
     }
     const float K = 1.000001f;
     const float delta = p.f32_delta;
@@ -255,22 +270,31 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
     unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     float* s_pf = reinterpret_cast<float*>(s_pair);
-    // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
-    uint32_t nf = 0;
-    float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
-    if (beg + tid < end) { nf = p.lf[beg + tid]; nv = p.f32[nf]; }
     const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
+    const uint64_t co = p.coff[s];               // ... and first 256-entry chunk sphere
+    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+#define qxf __uint_as_float((uint32_t)QX)
+#define qyf __uint_as_float((uint32_t)QY)
+#define qzf __uint_as_float((uint32_t)QZ)
     if (active && !p.no_seed && !p.no_batch) {
-        // Tighter seed: every face of batch b lies within |q - C_b| + R_b of q, so the min of that over
-        // the list's batch spheres bounds the distance to the mesh from above.  fp32 with upward
+        // Tighter seed: every face of a batch/chunk lies within |q - C| + R of q, so the min of that
+        // over the list's spheres bounds the distance to the mesh from above.  fp32 with upward
         // rounding: sqrt(d2f)*(1+1e-6) covers the rounding of d2f, delta the fp32 rounding of q
-        // (C_b is an exact float), and the stored radius is R*K rounded up (>= R).
+        // (C is an exact float), and the stored radius is R*K rounded up (>= R).  The min runs over
+        // every chunk sphere, then over the batch spheres of this lane's best chunk.
+        float ub = finf;
+        uint32_t bc = 0;
+        for (uint32_t c2 = 0; c2 < nch; ++c2) {
+            const float4 c = p.csph[co + c2];  // same address across the tile's lanes: broadcast
+            const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+            const float u = __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w);
+            if (u < ub) { ub = u; bc = c2; }
+        }
         const uint64_t nbl = p.boff[s + 1] - bo;
-        float ub = __int_as_float(0x7f800000);
-        const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY),
-                    qzf = __uint_as_float((uint32_t)QZ);
-        for (uint64_t b2 = 0; b2 < nbl; ++b2) {
-            const float4 c = p.bsph[bo + b2];  // same address across the tile's lanes: broadcast
+        const uint64_t bb0 = (uint64_t)bc * (kChunk / 32), bb1 = min(nbl, bb0 + kChunk / 32);
+        for (uint64_t b2 = bb0; b2 < bb1; ++b2) {
+            const float4 c = p.bsph[bo + b2];
             const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
             const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
             ub = fminf(ub, __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w));
@@ -282,66 +306,98 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
             DK = pk2(dkf, dkf);
         }
     }
-    for (uint64_t base = beg; base < end; base += kChunk) {
-        const int mc = (int)min((uint64_t)kChunk, end - base);
-        const int nb = (mc + 31) >> 5;
-        if (base != beg) __syncthreads();        // the previous chunk is fully consumed
-        // level 1: the enclosing sphere of each 32-entry batch.  If every lane's conservative fp32
-        // bound to it exceeds the lane's d_min, every member sphere's bound does too, so the whole
-        // batch is pruned exactly as the per-candidate tests would prune it (and is never staged).
-        if (tid < nb) s_bsph[tid] = p.bsph[bo + ((base - beg) >> 5) + tid];
-        if (tid == 0) s_need = 0u;
+    // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
+    uint32_t nf = 0;
+    float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
+    uint32_t pre_c = 0xffffffffu;                // chunk held in (nf, nv)
+    bool first_chunk = true;
+    for (uint32_t w0 = 0; w0 < nch; w0 += kWinChunks) {
+        const uint32_t wn = min(nch - w0, (uint32_t)kWinChunks);
+        const int nwords = (int)((wn + 31) >> 5);
+        // level 0: a chunk is scanned only if some row's conservative bound to its sphere does not
+        // exceed that row's d_min (any replica's d_min is a valid upper bound of the row's distance)
+        if (w0 != 0) __syncthreads();            // every thread is done with the previous window's order
+        if (tid < kWinChunks / 32) {
+            const int nv_ = min(32, max(0, (int)wn - 32 * tid));
+            const uint32_t vmask = nv_ == 32 ? 0xffffffffu : ((1u << nv_) - 1u);
+            s_cw[tid] = (p.no_batch || nch == 1) ? vmask : 0u;
+        }
         __syncthreads();
-        uint32_t wneed = 0;
-        if (warp_on) {
-            for (int bb = r; bb < nb; bb += R) {
-                bool need = p.no_batch != 0;
-                if (active && !need) {
-                    const float4 c = s_bsph[bb];
-                    float dkx, dky;
-                    upk2(DK, dkx, dky);
-                    const float dx = __uint_as_float((uint32_t)QX) - c.x;
-                    const float dy = __uint_as_float((uint32_t)QY) - c.y;
-                    const float dz = __uint_as_float((uint32_t)QZ) - c.z;
-                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                    const float th = __fadd_ru(c.w, dkx);
-                    need = !(d2f > __fmul_ru(th, th));
+        if (warp_on && !p.no_batch && nch > 1) {
+            float dkx, dky;
+            upk2(DK, dkx, dky);
+            for (int wi = r; wi < nwords; wi += R) {
+                uint32_t bits = 0;
+                const int kn = min(32, (int)wn - 32 * wi);
+                for (int k = 0; k < kn; ++k) {
+                    bool need = false;
+                    if (active) {
+                        const float4 c = p.csph[co + w0 + 32 * wi + k];
+                        const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+                        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                        const float th = __fadd_ru(c.w, dkx);
+                        need = !(d2f > __fmul_ru(th, th));
+                    }
+                    if (__any_sync(0xffffffffu, need)) bits |= 1u << k;
                 }
-                if (__any_sync(0xffffffffu, need)) wneed |= 1u << bb;
+                if (lane == 0 && bits) atomicOr(&s_cw[wi], bits);
             }
-            if (lane == 0 && wneed) atomicOr(&s_need, wneed);
         }
         __syncthreads();
-        const uint32_t cneed = s_need;
+        // Visit the needed chunks best-first for the tile's first row (every row of the tile lies in
+        // the same Voronoi cell): an early small d_min then prunes most later chunks at the batch
+        // level.  The order changes neither the (d^2, face id) argmin nor which faces may be skipped.
+        int nord;
         {
-            const int pp = tid >> 1, h = tid & 1;
-            if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
-            s_fid[tid] = nf;
-            if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the lower-bound record (rare path, broadcast)
-                const float4* lr = p.lbr + 4 * (uint64_t)nf;
-                s_lb[4 * tid] = lr[0];
-                s_lb[4 * tid + 1] = lr[1];
-                s_lb[4 * tid + 2] = lr[2];
-                s_lb[4 * tid + 3] = lr[3];
+            int pos = -1;
+            uint32_t key = 0;
+            if (tid < (int)wn) {
+                const uint32_t wb = s_cw[tid >> 5];
+                if ((wb >> (tid & 31)) & 1u) {
+                    pos = __popc(wb & ((1u << (tid & 31)) - 1u));
+                    for (int k = 0; k < (tid >> 5); ++k) pos += __popc(s_cw[k]);
+                    if (nch > 1) {
+                        const float4 c = p.csph[co + w0 + tid];
+                        const float4 qr = s_qrep;
+                        const float dx = qr.x - c.x, dy = qr.y - c.y, dz = qr.z - c.z;
+                        const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
+                        key = __float_as_uint(fmaxf(lb, 0.f));
+                    }
+                }
             }
-            s_pf[8 * pp + h] = nv.x;
-            s_pf[8 * pp + 2 + h] = nv.y;
-            s_pf[8 * pp + 4 + h] = nv.z;
-            s_pf[8 * pp + 6 + h] = nv.w;
+            nord = 0;
+            for (int k = 0; k < nwords; ++k) nord += __popc(s_cw[k]);
+            if (pos >= 0) { s_oidx[pos] = (uint32_t)tid; s_okey[pos] = key; }
+            __syncthreads();
+            if (nord > 1) {
+                uint32_t mi = 0, rank = 0;
+                if (tid < nord) {
+                    mi = s_oidx[tid];
+                    const uint32_t mk = s_okey[tid];
+                    for (int u = 0; u < nord; ++u) {
+                        const uint32_t ku = s_okey[u];
+                        rank += (ku < mk || (ku == mk && u < tid)) ? 1u : 0u;
+                    }
+                }
+                __syncthreads();
+                if (tid < nord) s_oidx[rank] = mi;
+                __syncthreads();
+            }
         }
-        __syncthreads();
-        // prefetch the next chunk while this one is scanned
-        const uint64_t nxt = base + kChunk + tid;
-        if (nxt < end) { nf = p.lf[nxt]; nv = p.f32[nf]; }
-        if (!warp_on) continue;
-        for (int bb = r; bb < nb; bb += R) {
-            if (!((wneed >> bb) & 1u)) continue;  // pruned whole by its batch sphere
-            const int k0 = bb * 32;
+        // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)},
+        // lb: 32 x 64-byte lower-bound records, fid: 32 face ids).  Each lane computes a pass/prune bit
+        // per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the warp
+        // walks the union of set bits in list order; a lane whose bit is set re-tests with its
+        // CURRENT d_min, applies the tight fp32 lower bound, and survivors run the exact fp64 kernel
+        // on the face record (all lanes read the same record: broadcast).  stage_lb: the lower-bound
+        // records of the union are loaded here (lane k holds entry k's face id my_f).
+        auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
+                              uint32_t my_f) {
             uint32_t mask = 0;
             if (active) {
 #pragma unroll
                 for (int pp = 0; pp < 16; ++pp) {
-                    const float4 A = s_pair[k0 + 2 * pp], B = s_pair[k0 + 2 * pp + 1];
+                    const float4 A = pair[2 * pp], B = pair[2 * pp + 1];
                     const uint64_t dx = sub2(QX, pk2(A.x, A.y));
                     const uint64_t dy = sub2(QY, pk2(A.z, A.w));
                     const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
@@ -354,49 +410,211 @@ __global__ void __launch_bounds__(kTile, 3) k_scan_tiles(Params p, const double*
                     mask |= (uint32_t)(!(d0 > t0)) << (2 * pp);
                     mask |= (uint32_t)(!(d1 > t1)) << (2 * pp + 1);
                 }
-                const int valid = mc - k0;
                 if (valid < 32) mask &= (1u << valid) - 1u;
             }
             uint32_t um = __reduce_or_sync(0xffffffffu, mask);
             if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
+            if (stage_lb && um) {
+                if ((um >> lane) & 1u) {
+                    const float4* lr = p.lbr + 4 * (uint64_t)my_f;
+                    lb[4 * lane] = lr[0];
+                    lb[4 * lane + 1] = lr[1];
+                    lb[4 * lane + 2] = lr[2];
+                    lb[4 * lane + 3] = lr[3];
+                }
+                __syncwarp();
+            }
+            const float* pf = reinterpret_cast<const float*>(pair);
+            // the exact test of one candidate kk of this lane, after re-testing with the CURRENT d_min
+            // (the batch mask used the d_min of the batch start): the same conservative fp32 sphere
+            // test, then the tight lower bound, then fp64
+            auto visit = [&](int kk) {
+                {
+                    const int pp = kk >> 1, h = kk & 1;
+                    float dkx, dky;
+                    upk2(DK, dkx, dky);
+                    const float dx = qxf - pf[8 * pp + h];
+                    const float dy = qyf - pf[8 * pp + 2 + h];
+                    const float dz = qzf - pf[8 * pp + 4 + h];
+                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                    const float th = __fadd_ru(pf[8 * pp + 6 + h], dkx);
+                    if (d2f > __fmul_ru(th, th)) return;
+                    const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
+                    if (lb2_face(lb + 4 * kk, qxf, qyf, qzf) > __fmul_ru(thl, thl)) return;
+                }
+                const uint32_t f = fid[kk];
+                V a, bb3, c3, pp3;
+                load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);
+                const double dd = closest_tri(q, a, bb3, c3, &pp3);
+                ++exact;
+                if (dd < best || (dd == best && f < bf)) {
+                    best = dd;
+                    bf = f;
+                    dmin = sqrt(dd);
+                    const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+                    DK = pk2(dkf, dkf);
+                }
+            };
+            // the warp walks the union of set bits in list order (the face record read is a broadcast)
             while (um) {
                 const int kk = __ffs(um) - 1;
                 um &= um - 1;
-                if ((mask >> kk) & 1u) {
-                    // the batch mask used the d_min of the batch start: re-test this candidate with
-                    // the current one (same conservative fp32 sphere test, operands already in smem)
-                    {
-                        const int k = k0 + kk, pp = k >> 1, h = k & 1;
+                if ((mask >> kk) & 1u) visit(kk);
+            }
+        };
+        if (G == 1) {
+            // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
+            // Warps pull batches of the ordered chunks from a shared counter and stage them in their
+            // own shared-memory slice -- no block barrier until the window ends, and the load
+            // balances itself (replica warps otherwise wait at every chunk for the slowest one).
+            if (tid == 0) s_next = 0u;
+            __syncthreads();
+            const uint32_t T = (uint32_t)nord * (kChunk / 32);
+            float4* wp = s_pair + 32 * w;
+            float* wpf = reinterpret_cast<float*>(wp);
+            uint32_t* wf = s_fid + 32 * w;
+            float4* wl = s_lb + 128 * w;
+            for (;;) {
+                uint32_t t = 0;
+                if (lane == 0) t = atomicAdd(&s_next, 1u);
+                t = __shfl_sync(0xffffffffu, t, 0);
+                if (t >= T) break;
+                const uint32_t cidx = w0 + s_oidx[t / (kChunk / 32)];
+                const uint32_t gb = cidx * (kChunk / 32) + t % (kChunk / 32);  // batch index in the list
+                const uint64_t b0 = beg + 32ull * gb;
+                if (b0 >= end) continue;
+                const int valid = (int)min((uint64_t)32, end - b0);
+                bool need = p.no_batch != 0;
+                if (active && !need) {
+                    const float4 c = p.bsph[bo + gb];
+                    float dkx, dky;
+                    upk2(DK, dkx, dky);
+                    const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                    const float th = __fadd_ru(c.w, dkx);
+                    need = !(d2f > __fmul_ru(th, th));
+                }
+                if (!__any_sync(0xffffffffu, need)) continue;  // pruned whole by its batch sphere
+                uint32_t f = 0;
+                float4 rv = make_float4(finf, 0.f, 0.f, 0.f);
+                if (lane < valid) { f = p.lfs[b0 + lane]; rv = p.f32[f]; }
+                wf[lane] = f;
+                {
+                    const int pp = lane >> 1, h = lane & 1;
+                    wpf[8 * pp + h] = rv.x;
+                    wpf[8 * pp + 2 + h] = rv.y;
+                    wpf[8 * pp + 4 + h] = rv.z;
+                    wpf[8 * pp + 6 + h] = rv.w;
+                }
+                __syncwarp();
+                scan_batch(wp, wl, wf, valid, true, f);
+                __syncwarp();                    // the slice is rewritten by the next batch
+            }
+            continue;                            // next window (its first barrier orders s_next)
+        }
+        for (int oi = 0; oi < nord; ++oi) {
+            const uint32_t cidx = w0 + s_oidx[oi];
+            const uint64_t base = beg + (uint64_t)cidx * kChunk;
+            const int mc = (int)min((uint64_t)kChunk, end - base);
+            const int nb = (mc + 31) >> 5;
+            if (!first_chunk) __syncthreads();   // the previous chunk is fully consumed
+            first_chunk = false;
+            if (pre_c != cidx) {
+                nf = 0;
+                nv = make_float4(finf, 0.f, 0.f, 0.f);
+                if (tid < mc) { nf = p.lfs[base + tid]; nv = p.f32[nf]; }
+            }
+            // level 1: the enclosing sphere of each 32-entry batch.  If every lane's conservative fp32
+            // bound to it exceeds the lane's d_min, every member sphere's bound does too, so the whole
+            // batch is pruned exactly as the per-candidate tests would prune it (and is never staged).
+            if (tid < nb) s_bsph[tid] = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + tid];
+            if (tid == 0) s_need = 0u;
+            __syncthreads();
+            uint32_t wneed = 0;
+            if (warp_on) {
+                for (int bb = r; bb < nb; bb += R) {
+                    bool need = p.no_batch != 0;
+                    if (active && !need) {
+                        const float4 c = s_bsph[bb];
                         float dkx, dky;
                         upk2(DK, dkx, dky);
-                        const float dx = __uint_as_float((uint32_t)QX) - s_pf[8 * pp + h];
-                        const float dy = __uint_as_float((uint32_t)QY) - s_pf[8 * pp + 2 + h];
-                        const float dz = __uint_as_float((uint32_t)QZ) - s_pf[8 * pp + 4 + h];
+                        const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
                         const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                        const float th = __fadd_ru(s_pf[8 * pp + 6 + h], dkx);
-                        if (d2f > __fmul_ru(th, th)) continue;
-                        // then the tight lower bound
-                        const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-                        if (lb2_face(s_lb + 4 * k, __uint_as_float((uint32_t)QX), __uint_as_float((uint32_t)QY),
-                                     __uint_as_float((uint32_t)QZ)) > __fmul_ru(thl, thl))
-                            continue;
+                        const float th = __fadd_ru(c.w, dkx);
+                        need = !(d2f > __fmul_ru(th, th));
                     }
-                    const uint32_t f = s_fid[k0 + kk];
-                    V a, bb3, c3, pp3;
-                    load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);  // same address across the warp
-                    const double dd = closest_tri(q, a, bb3, c3, &pp3);
-                    ++exact;
-                    if (dd < best || (dd == best && f < bf)) {
-                        best = dd;
-                        bf = f;
-                        dmin = sqrt(dd);
-                        const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
-                        DK = pk2(dkf, dkf);
-                    }
+                    if (__any_sync(0xffffffffu, need)) wneed |= 1u << bb;
                 }
+                if (lane == 0 && wneed) atomicOr(&s_need, wneed);
+            }
+            __syncthreads();
+            const uint32_t cneed = s_need;
+            // prefetch the window's next chunk while this one is scanned
+            auto prefetch_next = [&]() {
+                pre_c = 0xffffffffu;
+                if (oi + 1 < nord) {
+                    const uint32_t c2 = w0 + s_oidx[oi + 1];
+                    const uint64_t b2 = beg + (uint64_t)c2 * kChunk;
+                    nf = 0;
+                    nv = make_float4(finf, 0.f, 0.f, 0.f);
+                    if (b2 + tid < end) { nf = p.lfs[b2 + tid]; nv = p.f32[nf]; }
+                    pre_c = c2;
+                }
+            };
+            if (!cneed) {                        // every batch pruned with the current d_min
+                prefetch_next();
+                continue;
+            }
+            if (P2M_BATCH_ORDER && w == 0) {
+                // the chunk's batches best-first for the tile's first row (all rows share a cell)
+                uint32_t key = 0xffffffffu;
+                if (lane < nb) {
+                    const float4 c = s_bsph[lane];
+                    const float4 qr = s_qrep;
+                    const float dx = qr.x - c.x, dy = qr.y - c.y, dz = qr.z - c.z;
+                    const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
+                    key = __float_as_uint(fmaxf(lb, 0.f));
+                }
+                uint32_t rk = 0;
+#pragma unroll
+                for (int j = 0; j < kChunk / 32; ++j) {
+                    const uint32_t kj = __shfl_sync(0xffffffffu, key, j);
+                    rk += (kj < key || (kj == key && j < lane)) ? 1u : 0u;
+                }
+                if (lane < nb) s_bord[rk] = (uint8_t)lane;
+            }
+            {
+                const int pp = tid >> 1, h = tid & 1;
+                if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
+                s_fid[tid] = nf;
+                if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the lower-bound record (rare path, broadcast)
+                    const float4* lr = p.lbr + 4 * (uint64_t)nf;
+                    s_lb[4 * tid] = lr[0];
+                    s_lb[4 * tid + 1] = lr[1];
+                    s_lb[4 * tid + 2] = lr[2];
+                    s_lb[4 * tid + 3] = lr[3];
+                }
+                s_pf[8 * pp + h] = nv.x;
+                s_pf[8 * pp + 2 + h] = nv.y;
+                s_pf[8 * pp + 4 + h] = nv.z;
+                s_pf[8 * pp + 6 + h] = nv.w;
+            }
+            __syncthreads();
+            prefetch_next();
+            if (!warp_on) continue;
+            for (int pos = r; pos < nb; pos += R) {
+                const int bb = P2M_BATCH_ORDER ? (int)s_bord[pos] : pos;
+                // pruned whole by its batch sphere for every row (cneed: the union over the replicas'
+                // level-1 votes -- with the reordering a replica scans batches another one voted on)
+                if (!((cneed >> bb) & 1u)) continue;
+                const int k0 = bb * 32;
+                scan_batch(s_pair + k0, s_lb + 4 * k0, s_fid + k0, mc - k0, false, 0u);
             }
         }
     }
+#undef qxf
+#undef qyf
+#undef qzf
     if (R > 1) {
         __syncthreads();
         const int slot = r * G * 32 + j;

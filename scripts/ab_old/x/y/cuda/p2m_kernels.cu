@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) k_nearest(Params p, const double* __restr
     if (i >= n) return;
     const uint32_t row = rows ? rows[i] : (uint32_t)i;
     const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
-    site[row] = nearest_site_cl(p, q).id;
+    site[row] = nearest_site_any(p, q).id;
 }
 
 // ---- launchers ----

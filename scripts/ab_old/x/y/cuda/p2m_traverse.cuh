@@ -74,6 +74,81 @@ __device__ __forceinline__ NN nearest_site_cl(const Params& p, V q) {
     return r;
 }
 
+// DelaunayWalk nearest_site (REF/SPEC.md:476, 516; oracle/p2m_oracle.c orc_walk_nearest): greedy
+// descent on the Delaunay adjacency -- move to the neighbour with the smallest (d^2, id) while it
+// beats the current site -- warm-started from the first site listed in q's grid cell (site 0
+// outside the grid box).  If the final site has an exactly equidistant neighbour, the tie set is
+// flooded and its lowest id returned (up to 16 tied sites; beyond that the k-d tree answers).
+__device__ __forceinline__ NN nearest_site_walk(const Params& p, V q) {
+    uint32_t v = 0, c;
+    if (p.grid_off && grid_cell(p, q, &c)) {
+        const uint32_t b = p.grid_off[c];
+        if (b < p.grid_off[c + 1]) v = p.grid_site[b];
+    }
+    D4 sv = ldg4(p.site_pos + v);
+    double dv = vd2(q, V{sv.x, sv.y, sv.z});
+    uint32_t visited = 1;
+    bool tie = false;
+    for (;;) {
+        uint32_t bst = v;
+        double bd = dv;
+        tie = false;
+        const uint64_t k1 = p.adj_off[v + 1];
+        for (uint64_t k = p.adj_off[v]; k < k1; ++k) {
+            const uint32_t w = p.adj[k];
+            const D4 s = ldg4(p.site_pos + w);
+            const double d = vd2(q, V{s.x, s.y, s.z});
+            ++visited;
+            tie |= d == dv;
+            if (d < bd || (d == bd && w < bst)) { bst = w; bd = d; }
+        }
+        if (bst == v) break;
+        v = bst;
+        dv = bd;
+    }
+    uint32_t best = v;
+    if (tie) {
+        uint32_t set[16];
+        int n = 1, head = 0;
+        set[0] = v;
+        while (head < n) {
+            const uint32_t u = set[head++];
+            for (uint64_t k = p.adj_off[u]; k < p.adj_off[u + 1]; ++k) {
+                const uint32_t w = p.adj[k];
+                const D4 s = ldg4(p.site_pos + w);
+                ++visited;
+                if (vd2(q, V{s.x, s.y, s.z}) != dv) continue;
+                bool seen = false;
+                for (int i = 0; i < n; ++i) seen |= set[i] == w;
+                if (seen) continue;
+                if (n == 16) {
+                    NN r = nearest_site(p, q);
+                    r.visited += visited;
+                    return r;
+                }
+                set[n++] = w;
+                best = min(best, w);
+            }
+        }
+        sv = ldg4(p.site_pos + best);
+    } else {
+        sv = ldg4(p.site_pos + best);
+    }
+    NN r;
+    r.d2 = dv;
+    r.id = best;
+    r.visited = visited;
+    r.sentinel = ((uint64_t)__double_as_longlong(sv.w) & kSentinelBit) != 0;
+    return r;
+}
+
+// the engine's nearest_site strategy (P2M_NNS_*, include/p2m.h)
+__device__ __forceinline__ NN nearest_site_any(const Params& p, V q) {
+    if (p.nns == 2 && p.adj_off) return nearest_site_walk(p, q);
+    if (p.nns == 1) return nearest_site(p, q);
+    return nearest_site_cl(p, q);
+}
+
 // Exact global closest point by the fallback BVH (REF/SPEC.md:201-209, 491): lowest face id on
 // exact d^2 ties; a node is skipped only when its box is farther than best*(1+1e-12).
 __device__ __forceinline__ uint32_t bvh_closest(const Params& p, V q, double* best_out) {

@@ -262,3 +262,29 @@ def test_fp32_prefilters_stress(variant):
     r = P.Engine(h).batch_query(q)
     ref = O.OracleEngine(h.arrays()).batch_query(q)
     _compare(r, ref, len(q))
+
+
+@pytest.mark.parametrize("chunks", ["0", "1", "3", "7"])
+def test_host_api_chunk_schedules_identical(c2, chunks, monkeypatch):
+    """p2m_query pipelines host-buffer batches in chunks (geometric by default, P2M_E2E_CHUNKS=k
+    equal chunks); rows never depend on the chunking and equal the device-resident path."""
+    import torch
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 1_000_000, 700_000)
+    monkeypatch.setenv("P2M_E2E_CHUNKS", chunks)
+    r = P.Engine(h).batch_query(q)
+    monkeypatch.delenv("P2M_E2E_CHUNKS")
+    eng = P.Engine(h)
+    n = len(q)
+    dq = torch.from_numpy(q).cuda()
+    od = torch.empty(n, dtype=torch.float64, device="cuda")
+    oc = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    of, osi, ofl = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3))
+    vp = lambda t: C.c_void_p(t.data_ptr())
+    L.check(L.cuda().p2m_query_device(eng.handle, 0, vp(dq), n, vp(od), vp(oc), vp(of), vp(osi), vp(ofl),
+                                      None, None))
+    torch.cuda.synchronize()
+    assert r.distance.tobytes() == od.cpu().numpy().tobytes()
+    assert r.closest.tobytes() == oc.cpu().numpy().tobytes()
+    assert np.array_equal(r.face, of.cpu().numpy().view(np.uint32))
+    assert np.array_equal(r.site, osi.cpu().numpy().view(np.uint32))
