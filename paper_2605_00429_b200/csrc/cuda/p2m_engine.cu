@@ -917,8 +917,6 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         s->params.grid_site = s->grid_site;
         s->params.nns = P2M_NNS_GRID;
         s->params.tile_order = -1;
-        s->params.rpw_max = 8;
-        if (const char* v = std::getenv("P2M_RPW_MAX")) s->params.rpw_max = (uint32_t)std::atoi(v);
         if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
         s->params.adj = s->adj;

@@ -197,167 +197,6 @@ constexpr int kChunk = 256;
 constexpr int kWinChunks = 256;                  // level-0 need bits are computed per window of chunks
 static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 
-// ---- sparse tiles: one warp per row ---------------------------------------------------------
-// A tile with only a few rows cannot fill a CTA's lanes with rows, so each row gets a whole warp
-// that walks the row's list hierarchically with the lanes spread over LIST ENTRIES instead:
-// 32 chunk spheres per step (level 0, visited best-first), the 8 batch spheres of a chunk (level 1,
-// best-first), then 32 candidates of a batch at once (fp32 sphere test, tight fp32 lower bound, and
-// the exact fp64 kernel on every survivor in parallel), d_min updated after each batch by a warp
-// lexicographic (d^2, face id) reduction.  Same conservative tests as the tile path.
-__device__ __forceinline__ void warp_argmin(double& d, uint32_t& f) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
-        const uint32_t f2 = __shfl_xor_sync(0xffffffffu, f, o);
-        if (d2 < d || (d2 == d && f2 < f)) { d = d2; f = f2; }
-    }
-}
-
-template <bool kCounters>
-__device__ __noinline__ void scan_row_warp(const Params& p, const double* __restrict__ q_xyz, uint32_t row,
-                                           uint32_t s, const Out& o, int lane) {
-    const float K = 1.000001f;
-    const float delta = p.f32_delta;
-    const float finf = __int_as_float(0x7f800000);
-    const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
-    const float qx = (float)q.x, qy = (float)q.y, qz = (float)q.z;
-    double best = __longlong_as_double(0x7ff0000000000000ll);
-    uint32_t bf = 0xffffffffu;
-    float DK = finf;                             // ((d_min up + delta) * K) up, warp-uniform
-    uint32_t exact = 0;
-    unsigned long long passes = 0;
-    auto set_dk = [&](double dm) { DK = __fmul_ru(__fadd_ru(__double2float_ru(dm), delta), K); };
-    if (!p.no_seed) {
-        const D4 rf = ldg4(p.site_ref + s);
-        if (rf.w != 0.0) set_dk(sqrt(vd2(q, V{rf.x, rf.y, rf.z})));
-    }
-    // conservative "may some member be within d_min" test against a group sphere
-    auto near = [&](float4 c, float& lbkey) {
-        const float dx = qx - c.x, dy = qy - c.y, dz = qz - c.z;
-        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-        lbkey = fmaxf(__fsqrt_rn(d2f) - c.w, 0.f);
-        const float th = __fadd_ru(c.w, DK);
-        return !(d2f > __fmul_ru(th, th));
-    };
-    const uint64_t beg = p.off[s], end = p.off[s + 1];
-    const uint64_t bo = p.boff[s], co = p.coff[s];
-    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
-    if (!p.no_seed && !p.no_batch) {             // seed: min over chunk spheres of |q - C| + R
-        float ub = finf;
-        for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
-            if (c0 + lane < nch) {
-                const float4 c = p.csph[co + c0 + lane];
-                const float dx = qx - c.x, dy = qy - c.y, dz = qz - c.z;
-                const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                ub = fminf(ub, __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w));
-            }
-        }
-        ub = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(ub)));  // ub >= 0: uint order
-        const float cand = __fmul_ru(__fadd_ru(__fadd_ru(ub, delta), delta), K);
-        if (cand < DK) DK = cand;
-    }
-    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
-        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
-        float ckey = finf;
-        bool cneed = false;
-        if (c0 + lane < nch) {
-            cs = p.csph[co + c0 + lane];
-            cneed = p.no_batch || near(cs, ckey);
-        }
-        uint32_t cm = __ballot_sync(0xffffffffu, cneed);
-        while (cm) {
-            // best-first: the needed chunk with the smallest lower bound (ties: lowest slot)
-            const uint32_t myk = ((cm >> lane) & 1u) ? __float_as_uint(ckey) : 0xffffffffu;
-            const uint32_t mk = __reduce_min_sync(0xffffffffu, myk);
-            const int k = __ffs(__ballot_sync(0xffffffffu, myk == mk && ((cm >> lane) & 1u))) - 1;
-            cm &= ~(1u << k);
-            float dummy;
-            const bool still = __shfl_sync(0xffffffffu, (int)(p.no_batch || (lane == k && near(cs, dummy))), k);
-            if (!still) continue;                // pruned by the d_min found meanwhile
-            const uint32_t cidx = c0 + k;
-            const uint64_t cb = beg + (uint64_t)cidx * kChunk;
-            const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
-            float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
-            float bkey = finf;
-            bool bneed = false;
-            if (lane < nb) {
-                bs = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + lane];
-                bneed = p.no_batch || near(bs, bkey);
-            }
-            uint32_t bm = __ballot_sync(0xffffffffu, bneed);
-            while (bm) {
-                const uint32_t myb = ((bm >> lane) & 1u) ? __float_as_uint(bkey) : 0xffffffffu;
-                const uint32_t mb = __reduce_min_sync(0xffffffffu, myb);
-                const int j = __ffs(__ballot_sync(0xffffffffu, myb == mb && ((bm >> lane) & 1u))) - 1;
-                bm &= ~(1u << j);
-                const bool bstill = __shfl_sync(0xffffffffu, (int)(p.no_batch || (lane == j && near(bs, dummy))), j);
-                if (!bstill) continue;
-                const uint64_t e = cb + 32ull * j + lane;
-                bool pass = false;
-                uint32_t f = 0;
-                if (e < end) {
-                    f = p.lfs[e];
-                    const float4 r = p.f32[f];
-                    const float dx = qx - r.x, dy = qy - r.y, dz = qz - r.z;
-                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                    const float th = __fadd_ru(r.w, DK);
-                    pass = !(d2f > __fmul_ru(th, th));
-                    if (pass) {
-                        const float thl = __fmul_ru(__fadd_ru(DK, p.lb_margin), 1.000001f);
-                        pass = !(lb2_face(p.lbr + 4 * (uint64_t)f, qx, qy, qz) > __fmul_ru(thl, thl));
-                    }
-                }
-                if (kCounters) passes += pass ? 1u : 0u;
-                double dd = __longlong_as_double(0x7ff0000000000000ll);
-                uint32_t ff = 0xffffffffu;
-                if (pass) {
-                    V a, b3, c3, pp3;
-                    load_tri(p.rec + 4 * (uint64_t)f, &a, &b3, &c3);
-                    dd = closest_tri(q, a, b3, c3, &pp3);
-                    ff = f;
-                }
-                exact += __popc(__ballot_sync(0xffffffffu, pass));
-                warp_argmin(dd, ff);
-                if (dd < best || (dd == best && ff < bf)) {
-                    best = dd;
-                    bf = ff;
-                    set_dk(sqrt(dd));
-                }
-            }
-        }
-    }
-    if (lane == 0) {
-        V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
-             __longlong_as_double(0x7ff8000000000000ll)};
-        if (bf != 0xffffffffu) {
-            V a, b3, c3;
-            load_tri(p.rec + 4 * (uint64_t)bf, &a, &b3, &c3);
-            closest_tri(q, a, b3, c3, &cp);
-        }
-        o.dist[row] = sqrt(best);
-        o.cp[3 * (uint64_t)row] = cp.x;
-        o.cp[3 * (uint64_t)row + 1] = cp.y;
-        o.cp[3 * (uint64_t)row + 2] = cp.z;
-        o.face[row] = bf;
-        if (kCounters) {
-            if (o.per_query) {
-                o.per_query[3 * (uint64_t)row] = end - beg;
-                o.per_query[3 * (uint64_t)row + 1] = exact;
-            }
-            if (o.agg) {
-                atomicAdd(o.agg + 0, (unsigned long long)(end - beg));
-                atomicAdd(o.agg + 1, (unsigned long long)exact);
-            }
-        }
-    }
-    if (kCounters && o.agg) {
-        unsigned long long v = passes;
-#pragma unroll
-        for (int sh = 16; sh > 0; sh >>= 1) v += __shfl_down_sync(0xffffffffu, v, sh);
-        if (lane == 0) atomicAdd(o.agg + 4, v);
-    }
-}
-
 constexpr int kWarps = kTile / 32;
 
 #ifndef P2M_BATCH_ORDER
@@ -396,15 +235,6 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     const int m = (int)(stop - start);
     const uint32_t s = key[start];
     const long long t_start = p.tile_trace ? clock64() : 0;
-    if (m <= (int)p.rpw_max) {                   // sparse tile: one warp per row
-        for (int j2 = w; j2 < m; j2 += kWarps) scan_row_warp<kCounters>(p, q_xyz, rows[start + j2], s, o, lane);
-        if (p.tile_trace && tid == 0) {
-            unsigned long long* t = p.tile_trace + 4 * (uint64_t)b;
-            t[0] = s; t[1] = (unsigned long long)m; t[2] = p.off[s + 1] - p.off[s];
-            t[3] = (unsigned long long)(clock64() - t_start) << 8;
-        }
-        return;
-    }
     const int G = (m + 31) >> 5;
     const int R = max(1, kWarps / G);
     const int r = w / G;                         // replica of this warp (uniform per warp)
