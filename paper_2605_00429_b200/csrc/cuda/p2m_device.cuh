@@ -117,6 +117,7 @@ struct Params {
     const uint32_t* grid_site;
     int nns;                // P2M_NNS_* strategy of nearest_site
     int tile_order;         // scan launch order: 0 site order, 1 longest-first, 2 list-length buckets
+    uint32_t small_chunks;  // tiles of <= 32 rows and lists of <= this many chunks: one warp per tile (0: off)
     unsigned long long* tile_trace;  // debug (P2M_TILE_TRACE): per tile {site, rows, list length, cycles | sm}
     const uint64_t* adj_off;  // Delaunay adjacency CSR (nullptr: no DelaunayWalk)
     const uint32_t* adj;

@@ -169,6 +169,21 @@ void build_bvh(const double* tri, uint64_t nf, FlatBvh& out) {
     rec.go(0, (uint32_t)nf);
 }
 
+// Per-call working set of run_pipeline (keys/rows double buffers, CUB temp, tile arrays).
+struct Scratch {
+    uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
+    uint32_t *flag = nullptr, *tix = nullptr, *tiles = nullptr, *meta = nullptr, *tord = nullptr;
+    void* tmp = nullptr;
+    uint64_t n = 0, max_t = 0;
+    size_t tb = 0;
+};
+
+void free_scratch(Scratch& c) {
+    cudaFree(c.keys); cudaFree(c.rows); cudaFree(c.keys2); cudaFree(c.rows2); cudaFree(c.flag); cudaFree(c.tix);
+    cudaFree(c.tiles); cudaFree(c.meta); cudaFree(c.tord); cudaFree(c.tmp);
+    c = Scratch{};
+}
+
 struct Slot {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -194,12 +209,18 @@ struct Slot {
     static constexpr int kPipe = 4;
     cudaStream_t pipe[kPipe] = {};
     cudaStream_t h2d = nullptr, d2h = nullptr;  // one in-order copy stream per PCIe direction
+    // side streams of the small-tile scan, forked from / joined to the calling stream: [k] for the
+    // host-API pipe k, [kPipe] for device-buffer calls
+    cudaStream_t side[kPipe + 1] = {};
+    cudaEvent_t fork[kPipe + 1] = {}, join[kPipe + 1] = {};
     static constexpr int kMaxChunks = 64;
     std::vector<cudaEvent_t> cev;                // 3 per chunk: input landed, kernels done, output left
     cudaEvent_t t0 = nullptr;                    // P2M_E2E_TRACE origin
     struct Ws {
         double *q = nullptr, *dist = nullptr, *cp = nullptr;
         uint32_t *face = nullptr, *site = nullptr, *flags = nullptr;
+        Scratch sc;  // the chunk's pipeline scratch: persistent, so chunks on different streams never
+                     // wait on each other through the stream-ordered allocator's reuse dependencies
     } ws[kPipe];
     uint64_t cap = 0;
     cudaEvent_t agg_ready = nullptr;
@@ -241,9 +262,15 @@ void free_slot(Slot& s) {
     cudaFree(s.adj_off); cudaFree(s.adj);
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
+        free_scratch(w.sc);
     }
     for (auto& st : s.pipe) if (st) cudaStreamDestroy(st);
     if (s.h2d) cudaStreamDestroy(s.h2d);
+    for (int k = 0; k <= Slot::kPipe; ++k) {
+        if (s.side[k]) cudaStreamDestroy(s.side[k]);
+        if (s.fork[k]) cudaEventDestroy(s.fork[k]);
+        if (s.join[k]) cudaEventDestroy(s.join[k]);
+    }
     if (s.d2h) cudaStreamDestroy(s.d2h);
     for (auto& e : s.cev) if (e) cudaEventDestroy(e);
     s.cev.clear();
@@ -354,6 +381,11 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     for (auto& st : s.pipe) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking));
+    for (int k = 0; k <= Slot::kPipe; ++k) {
+        CK(cudaStreamCreateWithFlags(&s.side[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&s.fork[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s.join[k], cudaEventDisableTiming));
+    }
     CK(cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking));
     s.cev.assign(3 * Slot::kMaxChunks, nullptr);
     // timing-capable only under P2M_E2E_TRACE (per-chunk timeline on stderr)
@@ -398,12 +430,15 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     return P2M_OK;
 }
 
-int ensure_ws(Slot& s, uint64_t n) {
+int ensure_scratch(Scratch& c, uint64_t n, uint64_t n_sites);
+
+int ensure_ws(Slot& s, uint64_t n, uint64_t n_sites) {
     if (n <= s.cap) return P2M_OK;
     CK(cudaDeviceSynchronize());
     s.cap = 0;
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
+        free_scratch(w.sc);
         w = Slot::Ws{};
         CK(cudaMalloc(&w.q, 24 * n));
         CK(cudaMalloc(&w.dist, 8 * n));
@@ -411,43 +446,77 @@ int ensure_ws(Slot& s, uint64_t n) {
         CK(cudaMalloc(&w.face, 4 * n));
         CK(cudaMalloc(&w.site, 4 * n));
         CK(cudaMalloc(&w.flags, 4 * n));
+        int rc = ensure_scratch(w.sc, n, n_sites);
+        if (rc != P2M_OK) return rc;
     }
     s.cap = n;
     return P2M_OK;
 }
 
-// Morton keys -> sort -> fused query.  rows_out (optional) receives the sorted row order.
+size_t pipeline_tmp_bytes(uint64_t n, uint64_t max_t, bool lpt) {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int64_t)n, 0, 30, (cudaStream_t)0);
+    tb = std::max(tb, p2m::dev::tiles_tmp_bytes(n));
+    if (lpt) tb = std::max(tb, p2m::dev::tile_order_tmp_bytes(max_t));
+    return tb;
+}
+
+// Persistent scratch for calls of up to n rows (synchronous allocation: call before a pipeline).
+int ensure_scratch(Scratch& c, uint64_t n, uint64_t n_sites) {
+    if (n <= c.n) return P2M_OK;
+    free_scratch(c);
+    const uint64_t max_t = p2m::dev::max_tiles(n, n_sites);
+    c.tb = pipeline_tmp_bytes(n, max_t, true);
+    CK(cudaMalloc(&c.keys, 4 * n)); CK(cudaMalloc(&c.rows, 4 * n));
+    CK(cudaMalloc(&c.keys2, 4 * n)); CK(cudaMalloc(&c.rows2, 4 * n));
+    CK(cudaMalloc(&c.flag, 4 * n)); CK(cudaMalloc(&c.tix, 4 * n));
+    CK(cudaMalloc(&c.tiles, 4 * max_t)); CK(cudaMalloc(&c.meta, 16)); CK(cudaMalloc(&c.tord, 16 * max_t));
+    CK(cudaMalloc(&c.tmp, c.tb));
+    c.n = n;
+    c.max_t = max_t;
+    return P2M_OK;
+}
+
+// Morton keys -> sort -> descend -> regroup -> tile scan (or the fused per-row query).  sc: a
+// persistent scratch of >= n rows, else the working set comes from the stream-ordered allocator.
 int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2m::dev::Out& o, bool counters,
-                 cudaStream_t st, bool nearest_only, uint32_t* d_site_only, bool allow_prof = true) {
+                 cudaStream_t st, bool nearest_only, uint32_t* d_site_only, bool allow_prof = true,
+                 Scratch* sc = nullptr, int side = Slot::kPipe) {
     if (n >= (1ull << 32)) { set_err("p2m_query_device: at most 2^32-1 rows per call"); return P2M_ERR_INVALID; }
     CK(cudaSetDevice(s.dev));
     uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
     void* tmp = nullptr;
     uint32_t *flag = nullptr, *tix = nullptr, *tiles = nullptr, *meta = nullptr;
     const bool grouped = !nearest_only && E->scan_mode == P2M_SCAN_GROUPED;
-    size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, rows2, (int64_t)n, 0, 30, st));
-    tb = std::max(tb, p2m::dev::tiles_tmp_bytes(n));
     const uint64_t max_t = p2m::dev::max_tiles(n, E->n_sites);
     // launch order of the scan tiles (P2M_TILE_ORDER): measured on c2, longest-first wins below a
     // few million rows (the heaviest tiles otherwise start last and set the tail) and site order
     // above (neighbouring tiles share lists in L2); -1 = choose by batch size
     int order = s.params.tile_order;
     if (order < 0) order = n < (4ull << 20) ? 1 : 0;
-    const bool lpt = order != 0;
-    if (grouped && lpt) tb = std::max(tb, p2m::dev::tile_order_tmp_bytes(max_t));
+    const bool lpt = true;  // the launch order array (site order, LPT or buckets; small tiles last) always exists
     uint32_t* tord = nullptr;  // 4 x max_t: keys, sorted keys, tile ids, launch order
-    CK(cudaMallocAsync(&keys, 4 * n, st));
-    CK(cudaMallocAsync(&rows, 4 * n, st));
-    CK(cudaMallocAsync(&keys2, 4 * n, st));
-    CK(cudaMallocAsync(&rows2, 4 * n, st));
-    CK(cudaMallocAsync(&tmp, tb, st));
-    if (grouped) {
-        CK(cudaMallocAsync(&flag, 4 * n, st));
-        CK(cudaMallocAsync(&tix, 4 * n, st));
-        CK(cudaMallocAsync(&tiles, 4 * max_t, st));
-        CK(cudaMallocAsync(&meta, 16, st));
-        if (lpt) CK(cudaMallocAsync(&tord, 16 * max_t, st));
+    size_t tb = 0;
+    const bool own = sc == nullptr || sc->n < n;
+    if (!own) {
+        keys = sc->keys; rows = sc->rows; keys2 = sc->keys2; rows2 = sc->rows2; tmp = sc->tmp; tb = sc->tb;
+        flag = sc->flag; tix = sc->tix; tiles = sc->tiles; meta = sc->meta;
+        if (grouped && lpt) tord = sc->tord;
+    } else {
+        tb = pipeline_tmp_bytes(n, max_t, grouped && lpt);
+        CK(cudaMallocAsync(&keys, 4 * n, st));
+        CK(cudaMallocAsync(&rows, 4 * n, st));
+        CK(cudaMallocAsync(&keys2, 4 * n, st));
+        CK(cudaMallocAsync(&rows2, 4 * n, st));
+        CK(cudaMallocAsync(&tmp, tb, st));
+        if (grouped) {
+            CK(cudaMallocAsync(&flag, 4 * n, st));
+            CK(cudaMallocAsync(&tix, 4 * n, st));
+            CK(cudaMallocAsync(&tiles, 4 * max_t, st));
+            CK(cudaMallocAsync(&meta, 16, st));
+            if (lpt) CK(cudaMallocAsync(&tord, 16 * max_t, st));
+        }
     }
     const bool prof = allow_prof && E->profiling && s.recorded < Slot::kRing;
     cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * s.recorded] : nullptr;
@@ -486,7 +555,7 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
             CK(p2m::dev::launch_tile_order(prm, keys2, tiles, meta, max_t, tord, tord + max_t, tord + 2 * max_t,
                                            tord + 3 * max_t, tmp, tb, st));
         CK(p2m::dev::launch_scan_tiles(prm, d_q, rows, keys2, tiles, meta, tord ? tord + 3 * max_t : nullptr, n, o,
-                                       counters, st));
+                                       counters, st, s.side[side], s.fork[side], s.join[side]));
         if (trace) {
             std::vector<unsigned long long> h(4 * ntile_max);
             CK(cudaMemcpyAsync(h.data(), trace, 32 * ntile_max, cudaMemcpyDeviceToHost, st));
@@ -496,6 +565,7 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         }
         if (prof) CK(cudaEventRecord(ev[5], st));
     }
+    if (!own) return P2M_OK;
     CK(cudaFreeAsync(keys, st));
     CK(cudaFreeAsync(rows, st));
     CK(cudaFreeAsync(keys2, st));
@@ -917,6 +987,8 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         s->params.grid_site = s->grid_site;
         s->params.nns = P2M_NNS_GRID;
         s->params.tile_order = -1;
+        s->params.small_chunks = 2;  // measured on c2 (1, 2 > 4) and c5 (2 ~ 4 > 0)
+        if (const char* v = std::getenv("P2M_SMALL_CHUNKS")) s->params.small_chunks = (uint32_t)std::min(4, std::max(0, std::atoi(v)));
         if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
         s->params.adj = s->adj;
@@ -1054,7 +1126,7 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             }
             uint64_t maxlen = 0;
             for (uint64_t l : len_of) maxlen = std::max(maxlen, l);
-            int rc = ensure_ws(s, maxlen);
+            int rc = ensure_ws(s, maxlen, e->n_sites);
             if (rc != P2M_OK) return rc;
             if (cnt) {
                 CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.pipe[0]));
@@ -1076,7 +1148,7 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
                 CK(cudaStreamWaitEvent(st, ev_in, 0));
                 if (c >= (size_t)Slot::kPipe) CK(cudaStreamWaitEvent(st, s.cev[3 * (c - Slot::kPipe) + 2], 0));
                 p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
-                rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false);
+                rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false, &w.sc, k);
                 if (rc != P2M_OK) return rc;
                 CK(cudaEventRecord(ev_k, st));
                 CK(cudaStreamWaitEvent(s.d2h, ev_k, 0));

@@ -37,8 +37,11 @@ namespace {
 
 constexpr int kTile = 256;
 
+#ifndef P2M_DESC_MINB
+#define P2M_DESC_MINB 5   // 48 registers, 5 CTAs/SM: the descent is load-latency bound (measured 0.77 -> 0.67 ms on c2)
+#endif
 template <bool kCounters>
-__global__ void __launch_bounds__(256) k_descend(Params p, const double* __restrict__ q_xyz,
+__global__ void __launch_bounds__(256, P2M_DESC_MINB) k_descend(Params p, const double* __restrict__ q_xyz,
                                                  const uint32_t* __restrict__ rows, uint64_t n,
                                                  uint32_t* __restrict__ site_key, Out o) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,6 +125,7 @@ __global__ void __launch_bounds__(256) k_tile_flags(Params p, const uint32_t* __
     const bool last_valid = k < n_sites && (i + 1 == n || key[i + 1] >= n_sites);
     if (last_valid) meta[1] = (uint32_t)(i + 1);
     if (i == 0 && k >= n_sites) meta[1] = 0;
+    if (i == 0) meta[2] = 0;  // small tiles, counted by k_tile_keys
 }
 
 __global__ void __launch_bounds__(256) k_tile_write(const uint32_t* __restrict__ flag,
@@ -199,64 +203,108 @@ static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 
 constexpr int kWarps = kTile / 32;
 
-#ifndef P2M_BATCH_ORDER
-#define P2M_BATCH_ORDER 1   // block path: visit a chunk's batches best-first for the tile's first row
-#endif
-#ifndef P2M_SCAN_MINB
-#define P2M_SCAN_MINB 4  // resident CTAs per SM the register budget is sized for (measured: 4 > 3 > 2)
-#endif
+// One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)}, lb: 32 x
+// 64-byte lower-bound records, fid: 32 face ids), scanned for this lane's row.  Each lane computes a
+// pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
+// warp walks the union of set bits in list order; a lane whose bit is set re-tests with its CURRENT
+// d_min, applies the tight fp32 lower bound, and survivors run the exact fp64 kernel on the face
+// record (all lanes read the same record: broadcast).  stage_lb: the lower-bound records of the
+// union are loaded here (lane k holds entry k's face id my_f).  Called by every lane of the warp.
 template <bool kCounters>
-__global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
-                                                         const uint32_t* __restrict__ rows,
-                                                         const uint32_t* __restrict__ key,
-                                                         const uint32_t* __restrict__ tiles,
-                                                         const uint32_t* __restrict__ meta,
-                                                         const uint32_t* __restrict__ order, Out o) {
-    __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
-    __shared__ uint32_t s_fid[kChunk];
-    __shared__ float4 s_lb[kChunk * 4];          // the chunk's fp32 lower-bound records (64 B each)
-    __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
-    __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
-    __shared__ uint32_t s_cw[kWinChunks / 32];   // chunks of the current window some row must scan
-    __shared__ uint32_t s_oidx[kWinChunks];      // ... in visiting order
-    __shared__ uint32_t s_okey[kWinChunks];
-    __shared__ float4 s_qrep;                    // the tile's first row (fp32), for the visiting order
-    __shared__ uint32_t s_next;                  // small tiles: next batch of the window to scan
-    __shared__ uint8_t s_bord[kChunk / 32];      // block path: visiting order of the chunk's batches
-    __shared__ double s_rd[kTile];
-    __shared__ uint32_t s_rf[kTile];
-    __shared__ uint32_t s_re[kTile];
-    const uint32_t nt = meta[0];
-    const uint32_t b = order ? order[blockIdx.x] : blockIdx.x;  // tiles launch longest-first
-    if (b >= nt) return;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const uint32_t start = tiles[b];
-    const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
-    const int m = (int)(stop - start);
-    const uint32_t s = key[start];
-    const long long t_start = p.tile_trace ? clock64() : 0;
-    const int G = (m + 31) >> 5;
-    const int R = max(1, kWarps / G);
-    const int r = w / G;                         // replica of this warp (uniform per warp)
-    const int j = (w % G) * 32 + lane;
-    const bool warp_on = r < R;
-    const bool active = warp_on && j < m;
-    uint32_t row = 0;
-    V q{0, 0, 0};
-    uint64_t QX = 0, QY = 0, QZ = 0;
+__device__ __forceinline__ void scan_batch_row(const Params& p, bool active, const V& q, uint64_t QX, uint64_t QY,
+                                               uint64_t QZ, uint64_t& DK, double& best, double& dmin, uint32_t& bf,
+                                               uint32_t& exact, unsigned long long& passes,
+                                               unsigned long long& rare_iters, const float4* pair, float4* lb,
+                                               const uint32_t* fid, int valid, bool stage_lb, uint32_t my_f,
+                                               int lane) {
+    const float K = 1.000001f;
+    const float delta = p.f32_delta;
+    const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
+    uint32_t mask = 0;
     if (active) {
-        row = rows[start + j];
-        q = V{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
-        const float fx = (float)q.x, fy = (float)q.y, fz = (float)q.z;
-        QX = pk2(fx, fx); QY = pk2(fy, fy); QZ = pk2(fz, fz);
-        if (tid == 0) s_qrep = make_float4(fx, fy, fz, 0.f);
+#pragma unroll
+        for (int pp = 0; pp < 16; ++pp) {
+            const float4 A = pair[2 * pp], B = pair[2 * pp + 1];
+            const uint64_t dx = sub2(QX, pk2(A.x, A.y));
+            const uint64_t dy = sub2(QY, pk2(A.z, A.w));
+            const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
+            const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+            const uint64_t th = add2_up(pk2(B.z, B.w), DK);
+            const uint64_t t2 = mul2_up(th, th);
+            // prune iff d2 > t2, i.e. iff fl(t2 - d2) is negative: IEEE subtraction keeps the
+            // sign of the exact difference and gives +0 on equality (pass), and NaN from
+            // inf - inf (padding against an unset d_min) has its sign bit clear (pass, masked
+            // by valid) -- so one FADD2 and two funnel shifts collect the 32 prune bits
+            float x0, x1;
+            upk2(sub2(t2, d2), x0, x1);
+            mask = __funnelshift_l(__float_as_uint(x0), mask, 1);
+            mask = __funnelshift_l(__float_as_uint(x1), mask, 1);
+        }
+        mask = ~__brev(mask);  // bit k = candidate k passes
+        if (valid < 32) mask &= (1u << valid) - 1u;
     }
+    uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+    if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
+    if (stage_lb && um) {
+        if ((um >> lane) & 1u) {
+            const float4* lr = p.lbr + 4 * (uint64_t)my_f;
+            lb[4 * lane] = lr[0];
+            lb[4 * lane + 1] = lr[1];
+            lb[4 * lane + 2] = lr[2];
+            lb[4 * lane + 3] = lr[3];
+        }
+        __syncwarp();
+    }
+    const float* pf = reinterpret_cast<const float*>(pair);
+    // the exact test of one candidate kk of this lane, after re-testing with the CURRENT d_min
+    // (the batch mask used the d_min of the batch start): the same conservative fp32 sphere
+    // test, then the tight lower bound, then fp64
+    auto visit = [&](int kk) {
+        {
+            const int pp = kk >> 1, h = kk & 1;
+            float dkx, dky;
+            upk2(DK, dkx, dky);
+            const float dx = qxf - pf[8 * pp + h];
+            const float dy = qyf - pf[8 * pp + 2 + h];
+            const float dz = qzf - pf[8 * pp + 4 + h];
+            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+            const float th = __fadd_ru(pf[8 * pp + 6 + h], dkx);
+            if (d2f > __fmul_ru(th, th)) return;
+            const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
+            if (lb2_face(lb + 4 * kk, qxf, qyf, qzf) > __fmul_ru(thl, thl)) return;
+        }
+        const uint32_t f = fid[kk];
+        V a, bb3, c3, pp3;
+        load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);
+        const double dd = closest_tri(q, a, bb3, c3, &pp3);
+        ++exact;
+        if (dd < best || (dd == best && f < bf)) {
+            best = dd;
+            bf = f;
+            dmin = sqrt(dd);
+            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+            DK = pk2(dkf, dkf);
+        }
+    };
+    // the warp walks the union of set bits in list order (the face record read is a broadcast)
+    while (um) {
+        const int kk = __ffs(um) - 1;
+        um &= um - 1;
+        if ((mask >> kk) & 1u) visit(kk);
+    }
+}
+
+// d_min seeds of one row of site s (both are upper bounds of the distance to the mesh, so the
+// (d^2, face id) argmin and every face that could tie it survive every prune).
+__device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q, uint64_t QX, uint64_t QY,
+                                         uint64_t QZ, double& dmin, uint64_t& DK) {
     const float K = 1.000001f;
     const float delta = p.f32_delta;
     const float finf = __int_as_float(0x7f800000);
-    double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
-    uint64_t DK = pk2(finf, finf);               // (dmin_up + delta) * K, rounded up, both halves
-    if (active && !p.no_seed) {
+    const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
+    const uint64_t bo = p.boff[s], co = p.coff[s];
+    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+    if (!p.no_seed) {
         // Seed d_min with an upper bound of the distance to the mesh: |q - ref| for a point ref ON
         // the mesh (the site itself for a mesh vertex, proj(s, M) for an auxiliary site).  A face
         // whose lower bound exceeds it (plus the prune slack) cannot attain or tie the minimum, so
@@ -269,18 +317,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             DK = pk2(dkf, dkf);
         }
     }
-    uint32_t bf = 0xffffffffu;
-    uint32_t exact = 0;
-    unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
-    const uint64_t beg = p.off[s], end = p.off[s + 1];
-    float* s_pf = reinterpret_cast<float*>(s_pair);
-    const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
-    const uint64_t co = p.coff[s];               // ... and first 256-entry chunk sphere
-    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
-#define qxf __uint_as_float((uint32_t)QX)
-#define qyf __uint_as_float((uint32_t)QY)
-#define qzf __uint_as_float((uint32_t)QZ)
-    if (active && !p.no_seed && !p.no_batch) {
+    if (!p.no_seed && !p.no_batch) {
         // Tighter seed: every face of a batch/chunk lies within |q - C| + R of q, so the min of that
         // over the list's spheres bounds the distance to the mesh from above.  fp32 with upward
         // rounding: sqrt(d2f)*(1+1e-6) covers the rounding of d2f, delta the fp32 rounding of q
@@ -310,6 +347,241 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             DK = pk2(dkf, dkf);
         }
     }
+}
+
+// ---- small tiles: one warp per tile ----------------------------------------------------------
+// A tile of at most 32 rows whose list has at most kSmallChunks chunks is scanned by ONE warp (lanes
+// = rows) instead of a whole CTA, so a CTA works on 8 such tiles at once.  It runs on a side stream
+// concurrently with k_scan_tiles (whose CTAs skip these tiles), so neither waits for the other's tail.  Most of a small tile's
+// time is the latency of its dependent gathers (seeds, list entries, records), which the 8x more
+// tiles in flight per SM hide; the per-row semantics -- seeds, chunk and batch sphere prunes,
+// best-first visiting for the tile's first row, the batch scan -- are those of k_scan_tiles.
+constexpr uint32_t kSmallChunks = 4;
+
+#ifndef P2M_SMALL_MINB
+#define P2M_SMALL_MINB 4
+#endif
+template <bool kCounters>
+__global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, const double* __restrict__ q_xyz,
+                                                        const uint32_t* __restrict__ rows,
+                                                        const uint32_t* __restrict__ key,
+                                                        const uint32_t* __restrict__ tiles,
+                                                        const uint32_t* __restrict__ meta,
+                                                        const uint32_t* __restrict__ order, Out o) {
+    __shared__ float4 s_pair[kWarps][32];
+    __shared__ uint32_t s_fid[kWarps][32];
+    __shared__ float4 s_lb[kWarps][128];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t nt = meta[0], ns = meta[2];
+    const uint32_t ti = blockIdx.x * kWarps + w;
+    if (ti >= ns) return;                        // warp-uniform: no block barrier in this kernel
+    float4* wp = s_pair[w];
+    uint32_t* wf = s_fid[w];
+    float4* wl = s_lb[w];
+    const uint32_t b = order[nt - ns + ti];
+    const uint32_t start = tiles[b];
+    const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
+    const int m = (int)(stop - start);
+    const uint32_t s = key[start];
+    const bool active = lane < m;
+    const float finf = __int_as_float(0x7f800000);
+    uint32_t row = 0;
+    V q{0, 0, 0};
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    if (active) {
+        row = rows[start + lane];
+        q = V{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+        fx = (float)q.x; fy = (float)q.y; fz = (float)q.z;
+    }
+    const uint64_t QX = pk2(fx, fx), QY = pk2(fy, fy), QZ = pk2(fz, fz);
+    const float rx = __shfl_sync(0xffffffffu, fx, 0), ry = __shfl_sync(0xffffffffu, fy, 0),
+                rz = __shfl_sync(0xffffffffu, fz, 0);  // the tile's first row: visiting order
+    double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
+    uint64_t DK = pk2(finf, finf);
+    if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
+    uint32_t bf = 0xffffffffu, exact = 0;
+    unsigned long long passes = 0, rare_iters = 0;
+    const uint64_t beg = p.off[s], end = p.off[s + 1];
+    const uint64_t bo = p.boff[s], co = p.coff[s];
+    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+    // conservative "may some member be within d_min" test of this lane's row against a group sphere
+    auto near = [&](float4 c) {
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        const float dx = fx - c.x, dy = fy - c.y, dz = fz - c.z;
+        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+        const float th = __fadd_ru(c.w, dkx);
+        return !(d2f > __fmul_ru(th, th));
+    };
+    auto lbkey = [&](float4 c) {                 // lower bound for the first row, as an ordered key
+        const float dx = rx - c.x, dy = ry - c.y, dz = rz - c.z;
+        const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
+        return __float_as_uint(fmaxf(lb, 0.f));
+    };
+    // chunks best-first (<= 4: every lane ranks them identically)
+    uint32_t ck[kSmallChunks], ci[kSmallChunks];
+#pragma unroll
+    for (uint32_t c = 0; c < kSmallChunks; ++c) {
+        ck[c] = c < nch ? (nch > 1 ? lbkey(p.csph[co + c]) : 0u) : 0xffffffffu;
+        ci[c] = c;
+    }
+#pragma unroll
+    for (int i = 1; i < (int)kSmallChunks; ++i)
+#pragma unroll
+        for (int j = i; j > 0; --j)
+            if (ck[j] < ck[j - 1]) {
+                const uint32_t tk = ck[j]; ck[j] = ck[j - 1]; ck[j - 1] = tk;
+                const uint32_t tc = ci[j]; ci[j] = ci[j - 1]; ci[j - 1] = tc;
+            }
+    float* wpf = reinterpret_cast<float*>(wp);
+    for (uint32_t oc = 0; oc < nch; ++oc) {
+        const uint32_t cidx = ci[oc];
+        if (nch > 1 && !p.no_batch && !__any_sync(0xffffffffu, active && near(p.csph[co + cidx]))) continue;
+        const uint64_t cb = beg + (uint64_t)cidx * kChunk;
+        const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
+        // the chunk's batches best-first for the first row
+        float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t bk = 0xffffffffu;
+        if (lane < nb) {
+            bs = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + lane];
+            bk = lbkey(bs);
+        }
+        uint32_t rk = 0;
+#pragma unroll
+        for (int j = 0; j < kChunk / 32; ++j) {
+            const uint32_t kj = __shfl_sync(0xffffffffu, bk, j);
+            rk += (kj < bk || (kj == bk && j < lane)) ? 1u : 0u;
+        }
+        for (int pos = 0; pos < nb; ++pos) {
+            const int src = __ffs(__ballot_sync(0xffffffffu, lane < nb && rk == (uint32_t)pos)) - 1;
+            const float4 c = make_float4(__shfl_sync(0xffffffffu, bs.x, src), __shfl_sync(0xffffffffu, bs.y, src),
+                                         __shfl_sync(0xffffffffu, bs.z, src), __shfl_sync(0xffffffffu, bs.w, src));
+            if (!p.no_batch && !__any_sync(0xffffffffu, active && near(c))) continue;  // pruned whole
+            const uint64_t b0 = cb + 32ull * src;
+            const int valid = (int)min((uint64_t)32, end - b0);
+            uint32_t f = 0;
+            float4 rv = make_float4(finf, 0.f, 0.f, 0.f);
+            if (lane < valid) { f = p.lfs[b0 + lane]; rv = p.f32[f]; }
+            wf[lane] = f;
+            {
+                const int pp = lane >> 1, h = lane & 1;
+                wpf[8 * pp + h] = rv.x;
+                wpf[8 * pp + 2 + h] = rv.y;
+                wpf[8 * pp + 4 + h] = rv.z;
+                wpf[8 * pp + 6 + h] = rv.w;
+            }
+            __syncwarp();
+            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, dmin, bf, exact, passes, rare_iters, wp,
+                                      wl, wf, valid, true, f, lane);
+            __syncwarp();                        // the slice is rewritten by the next batch
+        }
+    }
+    if (active) {
+        V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+             __longlong_as_double(0x7ff8000000000000ll)};
+        if (bf != 0xffffffffu) {
+            V a, bb, c;
+            load_tri(p.rec + 4 * (uint64_t)bf, &a, &bb, &c);
+            closest_tri(q, a, bb, c, &cp);
+        }
+        o.dist[row] = sqrt(best);
+        o.cp[3 * (uint64_t)row] = cp.x;
+        o.cp[3 * (uint64_t)row + 1] = cp.y;
+        o.cp[3 * (uint64_t)row + 2] = cp.z;
+        o.face[row] = bf;
+        if (kCounters && o.per_query) {
+            o.per_query[3 * (uint64_t)row] = end - beg;
+            o.per_query[3 * (uint64_t)row + 1] = exact;
+        }
+    }
+    if (kCounters && o.agg) {
+        unsigned long long v0 = active ? (end - beg) : 0ull, v1 = active ? exact : 0u, v2 = passes, v3 = rare_iters;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            v0 += __shfl_down_sync(0xffffffffu, v0, sh);
+            v1 += __shfl_down_sync(0xffffffffu, v1, sh);
+            v2 += __shfl_down_sync(0xffffffffu, v2, sh);
+            v3 += __shfl_down_sync(0xffffffffu, v3, sh);
+        }
+        if (lane == 0) {
+            atomicAdd(o.agg + 0, v0);
+            atomicAdd(o.agg + 1, v1);
+            atomicAdd(o.agg + 4, v2);
+            atomicAdd(o.agg + 5, v3);
+        }
+    }
+}
+
+
+#ifndef P2M_BATCH_ORDER
+#define P2M_BATCH_ORDER 1   // block path: visit a chunk's batches best-first for the tile's first row
+#endif
+#ifndef P2M_SCAN_MINB
+#define P2M_SCAN_MINB 4  // resident CTAs per SM the register budget is sized for (measured: 4 > 3 > 2)
+#endif
+template <bool kCounters>
+__global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
+                                                         const uint32_t* __restrict__ rows,
+                                                         const uint32_t* __restrict__ key,
+                                                         const uint32_t* __restrict__ tiles,
+                                                         const uint32_t* __restrict__ meta,
+                                                         const uint32_t* __restrict__ order, Out o) {
+    __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
+    __shared__ uint32_t s_fid[kChunk];
+    __shared__ float4 s_lb[kChunk * 4];          // the chunk's fp32 lower-bound records (64 B each)
+    __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
+    __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
+    __shared__ uint32_t s_cw[kWinChunks / 32];   // chunks of the current window some row must scan
+    __shared__ uint32_t s_oidx[kWinChunks];      // ... in visiting order
+    __shared__ uint32_t s_okey[kWinChunks];
+    __shared__ float4 s_qrep;                    // the tile's first row (fp32), for the visiting order
+    __shared__ uint32_t s_next;                  // small tiles: next batch of the window to scan
+    __shared__ uint8_t s_bord[kChunk / 32];      // block path: visiting order of the chunk's batches
+    __shared__ double s_rd[kTile];
+    __shared__ uint32_t s_rf[kTile];
+    __shared__ uint32_t s_re[kTile];
+    const uint32_t nt = meta[0];
+    if (blockIdx.x >= nt - meta[2]) return;     // invalid, or a small tile (k_scan_small)
+    const uint32_t b = order[blockIdx.x];        // launch order: site order or longest-first
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t start = tiles[b];
+    const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
+    const int m = (int)(stop - start);
+    const uint32_t s = key[start];
+    const long long t_start = p.tile_trace ? clock64() : 0;
+    const int G = (m + 31) >> 5;
+    const int R = max(1, kWarps / G);
+    const int r = w / G;                         // replica of this warp (uniform per warp)
+    const int j = (w % G) * 32 + lane;
+    const bool warp_on = r < R;
+    const bool active = warp_on && j < m;
+    uint32_t row = 0;
+    V q{0, 0, 0};
+    uint64_t QX = 0, QY = 0, QZ = 0;
+    if (active) {
+        row = rows[start + j];
+        q = V{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+        const float fx = (float)q.x, fy = (float)q.y, fz = (float)q.z;
+        QX = pk2(fx, fx); QY = pk2(fy, fy); QZ = pk2(fz, fz);
+        if (tid == 0) s_qrep = make_float4(fx, fy, fz, 0.f);
+    }
+    const float K = 1.000001f;
+    const float delta = p.f32_delta;
+    const float finf = __int_as_float(0x7f800000);
+    double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
+    uint64_t DK = pk2(finf, finf);               // (dmin_up + delta) * K, rounded up, both halves
+    uint32_t bf = 0xffffffffu;
+    uint32_t exact = 0;
+    unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
+    const uint64_t beg = p.off[s], end = p.off[s + 1];
+    float* s_pf = reinterpret_cast<float*>(s_pair);
+    const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
+    const uint64_t co = p.coff[s];               // ... and first 256-entry chunk sphere
+    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+#define qxf __uint_as_float((uint32_t)QX)
+#define qyf __uint_as_float((uint32_t)QY)
+#define qzf __uint_as_float((uint32_t)QZ)
+    if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
     // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
     uint32_t nf = 0;
     float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
@@ -397,78 +669,8 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         // records of the union are loaded here (lane k holds entry k's face id my_f).
         auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
                               uint32_t my_f) {
-            uint32_t mask = 0;
-            if (active) {
-#pragma unroll
-                for (int pp = 0; pp < 16; ++pp) {
-                    const float4 A = pair[2 * pp], B = pair[2 * pp + 1];
-                    const uint64_t dx = sub2(QX, pk2(A.x, A.y));
-                    const uint64_t dy = sub2(QY, pk2(A.z, A.w));
-                    const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
-                    const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-                    const uint64_t th = add2_up(pk2(B.z, B.w), DK);
-                    const uint64_t t2 = mul2_up(th, th);
-                    // prune iff d2 > t2, i.e. iff fl(t2 - d2) is negative: IEEE subtraction keeps the
-                    // sign of the exact difference and gives +0 on equality (pass), and NaN from
-                    // inf - inf (padding against an unset d_min) has its sign bit clear (pass, masked
-                    // by valid) -- so one FADD2 and two funnel shifts collect the 32 prune bits
-                    float x0, x1;
-                    upk2(sub2(t2, d2), x0, x1);
-                    mask = __funnelshift_l(__float_as_uint(x0), mask, 1);
-                    mask = __funnelshift_l(__float_as_uint(x1), mask, 1);
-                }
-                mask = ~__brev(mask);  // bit k = candidate k passes
-                if (valid < 32) mask &= (1u << valid) - 1u;
-            }
-            uint32_t um = __reduce_or_sync(0xffffffffu, mask);
-            if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
-            if (stage_lb && um) {
-                if ((um >> lane) & 1u) {
-                    const float4* lr = p.lbr + 4 * (uint64_t)my_f;
-                    lb[4 * lane] = lr[0];
-                    lb[4 * lane + 1] = lr[1];
-                    lb[4 * lane + 2] = lr[2];
-                    lb[4 * lane + 3] = lr[3];
-                }
-                __syncwarp();
-            }
-            const float* pf = reinterpret_cast<const float*>(pair);
-            // the exact test of one candidate kk of this lane, after re-testing with the CURRENT d_min
-            // (the batch mask used the d_min of the batch start): the same conservative fp32 sphere
-            // test, then the tight lower bound, then fp64
-            auto visit = [&](int kk) {
-                {
-                    const int pp = kk >> 1, h = kk & 1;
-                    float dkx, dky;
-                    upk2(DK, dkx, dky);
-                    const float dx = qxf - pf[8 * pp + h];
-                    const float dy = qyf - pf[8 * pp + 2 + h];
-                    const float dz = qzf - pf[8 * pp + 4 + h];
-                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                    const float th = __fadd_ru(pf[8 * pp + 6 + h], dkx);
-                    if (d2f > __fmul_ru(th, th)) return;
-                    const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-                    if (lb2_face(lb + 4 * kk, qxf, qyf, qzf) > __fmul_ru(thl, thl)) return;
-                }
-                const uint32_t f = fid[kk];
-                V a, bb3, c3, pp3;
-                load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);
-                const double dd = closest_tri(q, a, bb3, c3, &pp3);
-                ++exact;
-                if (dd < best || (dd == best && f < bf)) {
-                    best = dd;
-                    bf = f;
-                    dmin = sqrt(dd);
-                    const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
-                    DK = pk2(dkf, dkf);
-                }
-            };
-            // the warp walks the union of set bits in list order (the face record read is a broadcast)
-            while (um) {
-                const int kk = __ffs(um) - 1;
-                um &= um - 1;
-                if ((mask >> kk) & 1u) visit(kk);
-            }
+            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, dmin, bf, exact, passes, rare_iters, pair,
+                                      lb, fid, valid, stage_lb, my_f, lane);
         };
         if (G == 1) {
             // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
@@ -688,6 +890,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     }
 }
 
+
 }  // namespace
 
 cudaError_t launch_descend(const Params& p, const double* q, const uint32_t* rows, uint64_t n, uint32_t* site_key,
@@ -741,23 +944,30 @@ uint64_t max_tiles(uint64_t n, uint64_t n_sites) { return std::min<uint64_t>(n, 
 // END of the site-sorted order -- launched last, they would set a tail of up to ~2.5 ms on c2.
 __global__ void __launch_bounds__(256) k_tile_keys(Params p, const uint32_t* __restrict__ key,
                                                    const uint32_t* __restrict__ tiles,
-                                                   const uint32_t* __restrict__ meta, uint32_t max_t,
+                                                   uint32_t* __restrict__ meta, uint32_t max_t,
                                                    uint32_t* __restrict__ tkey, uint32_t* __restrict__ tidx) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= max_t) return;
     const uint32_t nt = meta[0];
     uint32_t k = 0;
+    bool small = false;
     if (t < nt) {
         const uint32_t start = tiles[t];
         const uint32_t stop = (t + 1 < nt) ? tiles[t + 1] : meta[1];
         const uint32_t s = key[start];
         const uint64_t len0 = p.off[s + 1] - p.off[s];
         const uint64_t len = len0 < (1u << 20) ? len0 : (1u << 20);
-        if (p.tile_order == 1) k = (uint32_t)((len * (uint64_t)(stop - start + 16)) >> 4) + 1u;
-        else k = (uint32_t)(64 - __clzll((long long)len)) + 1u;  // bit length: coarse, keeps site order
+        small = stop - start <= 32u && p.coff[s + 1] - p.coff[s] <= p.small_chunks;
+        if (small) k = 1u;                       // after every CTA tile: k_scan_small's range
+        else if (p.tile_order == 1) k = (uint32_t)((len * (uint64_t)(stop - start + 16)) >> 4) + 2u;
+        else if (p.tile_order == 2) k = (uint32_t)(64 - __clzll((long long)len)) + 2u;  // coarse buckets
+        else k = 2u;                             // site order (the sort is stable)
     }  // invalid tiles keep 0: launched last (and exit at once)
-    tkey[t] = k;
-    tidx[t] = t;
+    if (t < max_t) {
+        tkey[t] = k;
+        tidx[t] = t;
+    }
+    const uint32_t nsm = __popc(__ballot_sync(0xffffffffu, small));
+    if ((threadIdx.x & 31) == 0 && nsm) atomicAdd(meta + 2, nsm);
 }
 
 size_t tile_order_tmp_bytes(uint64_t max_t) {
@@ -767,7 +977,7 @@ size_t tile_order_tmp_bytes(uint64_t max_t) {
     return b;
 }
 
-cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32_t* tiles, const uint32_t* meta,
+cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32_t* tiles, uint32_t* meta,
                               uint64_t max_t, uint32_t* tkey, uint32_t* tkey2, uint32_t* tidx, uint32_t* order,
                               void* tmp, size_t tmp_bytes, cudaStream_t s) {
     if (!max_t) return cudaSuccess;
@@ -775,16 +985,32 @@ cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     size_t tb = tmp_bytes;
-    return cub::DeviceRadixSort::SortPairsDescending(tmp, tb, tkey, tkey2, tidx, order, (int64_t)max_t, 0, 32, s);
+    const int bits = p.tile_order == 1 ? 32 : p.tile_order == 2 ? 8 : 2;  // key ranges of k_tile_keys
+    return cub::DeviceRadixSort::SortPairsDescending(tmp, tb, tkey, tkey2, tidx, order, (int64_t)max_t, 0, bits, s);
 }
 
 cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* rows, const uint32_t* key,
                               const uint32_t* tiles, const uint32_t* meta, const uint32_t* order, uint64_t n,
-                              const Out& o, bool counters, cudaStream_t s) {
+                              const Out& o, bool counters, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
+                              cudaEvent_t join) {
     if (!n) return cudaSuccess;
+    if (!order) return cudaErrorInvalidValue;   // the launch order (launch_tile_order) is required
     const unsigned g = (unsigned)max_tiles(n, p.n_nodes);
+    cudaError_t e;
+    const bool small = p.small_chunks && side;
+    if (small) {                                 // fork: small tiles on the side stream
+        if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
+        const unsigned gs = (g + kWarps - 1) / kWarps;
+        if (counters) k_scan_small<true><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_small<false><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(join, side)) != cudaSuccess) return e;
+    }
     if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
     else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (small && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;  // join
     return cudaGetLastError();
 }
 

@@ -35,7 +35,7 @@ cudaError_t launch_descend(const Params& p, const double* q, const uint32_t* row
 size_t tiles_tmp_bytes(uint64_t n);
 uint64_t max_tiles(uint64_t n, uint64_t n_sites);
 size_t tile_order_tmp_bytes(uint64_t max_t);
-cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32_t* tiles, const uint32_t* meta,
+cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32_t* tiles, uint32_t* meta,
                               uint64_t max_t, uint32_t* tkey, uint32_t* tkey2, uint32_t* tidx, uint32_t* order,
                               void* tmp, size_t tmp_bytes, cudaStream_t s);
 cudaError_t launch_tiles(const Params& p, const uint32_t* key, uint64_t n, uint32_t n_sites, uint32_t* hpos, uint32_t* run_start,
@@ -43,7 +43,8 @@ cudaError_t launch_tiles(const Params& p, const uint32_t* key, uint64_t n, uint3
                          cudaStream_t s);
 cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* rows, const uint32_t* key,
                               const uint32_t* tiles, const uint32_t* meta, const uint32_t* order, uint64_t n,
-                              const Out& o, bool counters, cudaStream_t s);
+                              const Out& o, bool counters, cudaStream_t s, cudaStream_t side = nullptr,
+                              cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 
 }  // namespace dev
 }  // namespace p2m

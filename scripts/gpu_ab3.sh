@@ -1,1 +1,11 @@
-VARIANTS="head|| rpw0|-DP2M_RPW=0| oldmask|-DP2M_OLD_MASK| both|-DP2M_RPW=0,-DP2M_OLD_MASK|" CFGS="2 1" STEPS=10 bash scripts/gpu_ab.sh
+for sc in 1 2 4; do
+for n in 10000000 1000000 312500; do
+P2M_SMALL_CHUNKS=$sc python bench.py --config 2 --queries $n --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/hv.json 2>/dev/null
+python -c "
+import json; d=json.load(open('gpurun_out/hv.json')); s=d['config']['split_ms']; print('sc $sc n $n', round(d['value']/1e6,1), 'scan', round(s['scan'],3), 'e2e', round(d['e2e']['value']/1e6,1))"
+done; done
+for sc in 0 2 4; do
+P2M_SMALL_CHUNKS=$sc python bench.py --config 5 --queries 20000000 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/hv.json 2>/dev/null
+python -c "
+import json; d=json.load(open('gpurun_out/hv.json')); s=d['config']['split_ms']; print('c5 sc $sc', round(d['value']/1e6,1), 'scan', round(s['scan'],3), 'e2e', round(d['e2e']['value']/1e6,1))"
+done

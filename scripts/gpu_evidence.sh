@@ -18,6 +18,7 @@ timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_
     -o $O/prof_c2 python scripts/prof_run.py --config 2 --reps 2 > $O/ncu_full.log 2>&1
 tail -n 2 $O/ncu_launch.log $O/ncu_full.log
 for cfg in 1 ${CFGS:-}; do
-  timeout 900 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > $O/bench_c$cfg.json 2> $O/bench_c$cfg.err
+  st=10; [ "$cfg" -ge 3 ] && st=3
+  timeout 1500 python bench.py --config $cfg --steps $st --warmup 3 --e2e-steps 2 > $O/bench_c$cfg.json 2> $O/bench_c$cfg.err
   tail -c 300 $O/bench_c$cfg.json
 done
