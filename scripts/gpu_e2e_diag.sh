@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests -m "gpu and not slow" -x -q 2>&1 | tail -2
+
 for v in "" "P2M_E2E_CHUNKS=4" "P2M_E2E_CHUNKS=8" "P2M_E2E_CHUNKS=16"; do
   env $v P2M_E2E_TRACE=1 python bench.py --config 2 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 5 > gpurun_out/e2e.json 2>gpurun_out/e2e.err
   grep "e2e chunk" gpurun_out/e2e.err | tail -${TR:-0}
