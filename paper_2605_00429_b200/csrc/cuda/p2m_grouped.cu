@@ -592,72 +592,75 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         const int nwords = (int)((wn + 31) >> 5);
         // level 0: a chunk is scanned only if some row's conservative bound to its sphere does not
         // exceed that row's d_min (any replica's d_min is a valid upper bound of the row's distance)
-        if (w0 != 0) __syncthreads();            // every thread is done with the previous window's order
-        if (tid < kWinChunks / 32) {
-            const int nv_ = min(32, max(0, (int)wn - 32 * tid));
-            const uint32_t vmask = nv_ == 32 ? 0xffffffffu : ((1u << nv_) - 1u);
-            s_cw[tid] = (p.no_batch || nch == 1) ? vmask : 0u;
-        }
-        __syncthreads();
-        if (warp_on && !p.no_batch && nch > 1) {
-            float dkx, dky;
-            upk2(DK, dkx, dky);
-            for (int wi = r; wi < nwords; wi += R) {
-                uint32_t bits = 0;
-                const int kn = min(32, (int)wn - 32 * wi);
-                for (int k = 0; k < kn; ++k) {
-                    bool need = false;
-                    if (active) {
-                        const float4 c = p.csph[co + w0 + 32 * wi + k];
-                        const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
-                        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                        const float th = __fadd_ru(c.w, dkx);
-                        need = !(d2f > __fmul_ru(th, th));
-                    }
-                    if (__any_sync(0xffffffffu, need)) bits |= 1u << k;
-                }
-                if (lane == 0 && bits) atomicOr(&s_cw[wi], bits);
+        // a single-chunk list (most tiles) has a trivial window: no votes, no ordering, no barriers
+        int nord = 1;
+        if (nch > 1) {
+            if (w0 != 0) __syncthreads();            // every thread is done with the previous window's order
+            if (tid < kWinChunks / 32) {
+                const int nv_ = min(32, max(0, (int)wn - 32 * tid));
+                const uint32_t vmask = nv_ == 32 ? 0xffffffffu : ((1u << nv_) - 1u);
+                s_cw[tid] = (p.no_batch || nch == 1) ? vmask : 0u;
             }
-        }
-        __syncthreads();
-        // Visit the needed chunks best-first for the tile's first row (every row of the tile lies in
-        // the same Voronoi cell): an early small d_min then prunes most later chunks at the batch
-        // level.  The order changes neither the (d^2, face id) argmin nor which faces may be skipped.
-        int nord;
-        {
-            int pos = -1;
-            uint32_t key = 0;
-            if (tid < (int)wn) {
-                const uint32_t wb = s_cw[tid >> 5];
-                if ((wb >> (tid & 31)) & 1u) {
-                    pos = __popc(wb & ((1u << (tid & 31)) - 1u));
-                    for (int k = 0; k < (tid >> 5); ++k) pos += __popc(s_cw[k]);
-                    if (nch > 1) {
-                        const float4 c = p.csph[co + w0 + tid];
-                        const float4 qr = s_qrep;
-                        const float dx = qr.x - c.x, dy = qr.y - c.y, dz = qr.z - c.z;
-                        const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
-                        key = __float_as_uint(fmaxf(lb, 0.f));
-                    }
-                }
-            }
-            nord = 0;
-            for (int k = 0; k < nwords; ++k) nord += __popc(s_cw[k]);
-            if (pos >= 0) { s_oidx[pos] = (uint32_t)tid; s_okey[pos] = key; }
             __syncthreads();
-            if (nord > 1) {
-                uint32_t mi = 0, rank = 0;
-                if (tid < nord) {
-                    mi = s_oidx[tid];
-                    const uint32_t mk = s_okey[tid];
-                    for (int u = 0; u < nord; ++u) {
-                        const uint32_t ku = s_okey[u];
-                        rank += (ku < mk || (ku == mk && u < tid)) ? 1u : 0u;
+            if (warp_on && !p.no_batch && nch > 1) {
+                float dkx, dky;
+                upk2(DK, dkx, dky);
+                for (int wi = r; wi < nwords; wi += R) {
+                    uint32_t bits = 0;
+                    const int kn = min(32, (int)wn - 32 * wi);
+                    for (int k = 0; k < kn; ++k) {
+                        bool need = false;
+                        if (active) {
+                            const float4 c = p.csph[co + w0 + 32 * wi + k];
+                            const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+                            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                            const float th = __fadd_ru(c.w, dkx);
+                            need = !(d2f > __fmul_ru(th, th));
+                        }
+                        if (__any_sync(0xffffffffu, need)) bits |= 1u << k;
+                    }
+                    if (lane == 0 && bits) atomicOr(&s_cw[wi], bits);
+                }
+            }
+            __syncthreads();
+            // Visit the needed chunks best-first for the tile's first row (every row of the tile lies in
+            // the same Voronoi cell): an early small d_min then prunes most later chunks at the batch
+            // level.  The order changes neither the (d^2, face id) argmin nor which faces may be skipped.
+            {
+                int pos = -1;
+                uint32_t key = 0;
+                if (tid < (int)wn) {
+                    const uint32_t wb = s_cw[tid >> 5];
+                    if ((wb >> (tid & 31)) & 1u) {
+                        pos = __popc(wb & ((1u << (tid & 31)) - 1u));
+                        for (int k = 0; k < (tid >> 5); ++k) pos += __popc(s_cw[k]);
+                        if (nch > 1) {
+                            const float4 c = p.csph[co + w0 + tid];
+                            const float4 qr = s_qrep;
+                            const float dx = qr.x - c.x, dy = qr.y - c.y, dz = qr.z - c.z;
+                            const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
+                            key = __float_as_uint(fmaxf(lb, 0.f));
+                        }
                     }
                 }
+                nord = 0;
+                for (int k = 0; k < nwords; ++k) nord += __popc(s_cw[k]);
+                if (pos >= 0) { s_oidx[pos] = (uint32_t)tid; s_okey[pos] = key; }
                 __syncthreads();
-                if (tid < nord) s_oidx[rank] = mi;
-                __syncthreads();
+                if (nord > 1) {
+                    uint32_t mi = 0, rank = 0;
+                    if (tid < nord) {
+                        mi = s_oidx[tid];
+                        const uint32_t mk = s_okey[tid];
+                        for (int u = 0; u < nord; ++u) {
+                            const uint32_t ku = s_okey[u];
+                            rank += (ku < mk || (ku == mk && u < tid)) ? 1u : 0u;
+                        }
+                    }
+                    __syncthreads();
+                    if (tid < nord) s_oidx[rank] = mi;
+                    __syncthreads();
+                }
             }
         }
         // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)},
@@ -689,7 +692,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 if (lane == 0) t = atomicAdd(&s_next, 1u);
                 t = __shfl_sync(0xffffffffu, t, 0);
                 if (t >= T) break;
-                const uint32_t cidx = w0 + s_oidx[t / (kChunk / 32)];
+                const uint32_t cidx = w0 + (nch > 1 ? s_oidx[t / (kChunk / 32)] : 0u);
                 const uint32_t gb = cidx * (kChunk / 32) + t % (kChunk / 32);  // batch index in the list
                 const uint64_t b0 = beg + 32ull * gb;
                 if (b0 >= end) continue;
@@ -723,7 +726,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             continue;                            // next window (its first barrier orders s_next)
         }
         for (int oi = 0; oi < nord; ++oi) {
-            const uint32_t cidx = w0 + s_oidx[oi];
+            const uint32_t cidx = w0 + (nch > 1 ? s_oidx[oi] : 0u);
             const uint64_t base = beg + (uint64_t)cidx * kChunk;
             const int mc = (int)min((uint64_t)kChunk, end - base);
             const int nb = (mc + 31) >> 5;
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             auto prefetch_next = [&]() {
                 pre_c = 0xffffffffu;
                 if (oi + 1 < nord) {
-                    const uint32_t c2 = w0 + s_oidx[oi + 1];
+                    const uint32_t c2 = w0 + (nch > 1 ? s_oidx[oi + 1] : 0u);
                     const uint64_t b2 = beg + (uint64_t)c2 * kChunk;
                     nf = 0;
                     nv = make_float4(finf, 0.f, 0.f, 0.f);
