@@ -288,3 +288,28 @@ def test_host_api_chunk_schedules_identical(c2, chunks, monkeypatch):
     assert r.closest.tobytes() == oc.cpu().numpy().tobytes()
     assert np.array_equal(r.face, of.cpu().numpy().view(np.uint32))
     assert np.array_equal(r.site, osi.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("env", [
+    {"P2M_SMALL_CHUNKS": "0"},                 # every tile on the CTA path
+    {"P2M_SMALL_CHUNKS": "4"},                 # more tiles one warp per tile (side-stream kernel)
+    {"P2M_TILE_ORDER": "0"}, {"P2M_TILE_ORDER": "1"}, {"P2M_TILE_ORDER": "2"},  # launch orders
+    {"P2M_MORTON_BITS": "30"}, {"P2M_MORTON_BITS": "9"},  # finer / much coarser Morton order
+    {"P2M_LONG_TILE": "128"},                  # heavy-site tile height
+])
+def test_scan_schedules_identical(c2, env, monkeypatch):
+    """The tile partition (CTA tiles vs one-warp small tiles), their launch order, the Morton
+    granularity and the heavy-tile height change which warps scan what and in which order -- never
+    the rows: every schedule equals the default one and the oracle bit for bit.  400 k rows leave
+    ~23 rows per site, so small tiles dominate."""
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 2_000_000, 400_000)
+    base = P.Engine(h).batch_query(q)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    r = P.Engine(h).batch_query(q)
+    ref = {"site": base.site, "face": base.face, "flags": base.flags, "distance": base.distance,
+           "closest": base.closest}
+    _compare(r, ref, len(q))
+    if env == {"P2M_SMALL_CHUNKS": "4"}:
+        _compare(r, O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE), len(q))
