@@ -1,5 +1,5 @@
 # A/B: build variant libraries on the box and bench each (same workload, same box).
-# usage: VARIANTS="base|| minb2|-DP2M_SCAN_MINB=2| old||scripts/ab_old/x/y/cuda" CFGS="2 3" bash scripts/gpu_ab.sh
+# usage: VARIANTS="base|| minb2|-DP2M_SCAN_MINB=2| old||.ab/<commit>/x/y/cuda (git archive <commit> into .ab/, git-ignored)" CFGS="2 3" bash scripts/gpu_ab.sh
 # entry = name|NVEXTRA|CUDADIR (CUDADIR empty = current sources); env ENV_<name> is exported for that variant
 set -u
 for v in ${VARIANTS}; do

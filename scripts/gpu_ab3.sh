@@ -1,3 +1,6 @@
-timeout 900 python -m pytest tests -m "gpu and not slow" -x -q 2>&1 | tail -1
-VARIANTS="base||.ab/cur/x/y/cuda new||" CFGS="2 1" STEPS=10 bash scripts/gpu_ab.sh 2>&1
-for v in base new; do P2M_LIB_DIR=/tmp/p2m_ab_$v python bench.py --config 2 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$v descend', round(d['config']['split_ms']['descend'],3), round(d['value']/1e6,1))"; done
+for hd in 0 500 1500 4000; do
+for c in "1 0" "2 0" "2 2500000" "2 625000"; do set -- $c
+P2M_HEAVY_DIV=$hd python bench.py --config $1 --queries $2 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/hv.json 2>/dev/null
+python -c "
+import json; d=json.load(open('gpurun_out/hv.json')); s=d['config']['split_ms']; print('hd $hd c$1 n $2', round(d['value']/1e6,1), 'scan', round(s['scan'],3), 'e2e', round(d['e2e']['value']/1e6,1))"
+done; done
