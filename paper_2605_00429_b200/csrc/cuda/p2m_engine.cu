@@ -213,6 +213,8 @@ struct Slot {
     // host-API pipe k, [kPipe] for device-buffer calls
     cudaStream_t side[kPipe + 1] = {};
     cudaEvent_t fork[kPipe + 1] = {}, join[kPipe + 1] = {};
+    std::mutex side_mu;  // device-buffer calls from several host threads share side[kPipe]: the
+                         // fork/join event records and waits of one call must not interleave
     static constexpr int kMaxChunks = 64;
     std::vector<cudaEvent_t> cev;                // 3 per chunk: input landed, kernels done, output left
     cudaEvent_t t0 = nullptr;                    // P2M_E2E_TRACE origin
@@ -557,8 +559,12 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         if (tord)
             CK(p2m::dev::launch_tile_order(prm, keys2, tiles, meta, max_t, tord, tord + max_t, tord + 2 * max_t,
                                            tord + 3 * max_t, tmp, tb, st));
-        CK(p2m::dev::launch_scan_tiles(prm, d_q, rows, keys2, tiles, meta, tord ? tord + 3 * max_t : nullptr, n, o,
-                                       counters, st, s.side[side], s.fork[side], s.join[side]));
+        {
+            std::unique_lock<std::mutex> lk(s.side_mu, std::defer_lock);
+            if (side == Slot::kPipe) lk.lock();  // host-API pipes run under the slot mutex already
+            CK(p2m::dev::launch_scan_tiles(prm, d_q, rows, keys2, tiles, meta, tord ? tord + 3 * max_t : nullptr, n,
+                                           o, counters, st, s.side[side], s.fork[side], s.join[side]));
+        }
         if (trace) {
             std::vector<unsigned long long> h(4 * ntile_max);
             CK(cudaMemcpyAsync(h.data(), trace, 32 * ntile_max, cudaMemcpyDeviceToHost, st));

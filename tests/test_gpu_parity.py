@@ -313,3 +313,44 @@ def test_scan_schedules_identical(c2, env, monkeypatch):
     _compare(r, ref, len(q))
     if env == {"P2M_SMALL_CHUNKS": "4"}:
         _compare(r, O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE), len(q))
+
+
+def test_concurrent_device_calls_one_engine(c2):
+    """One engine queried from several host threads at once, each on its own stream
+    (REF/SPEC.md:518-519: queries are pure and concurrent): the fork/join of the small-tile side
+    stream must not interleave between calls.  Every thread's rows equal the serial answer."""
+    import threading
+    import torch
+    V, F, h = c2
+    eng = P.Engine(h)
+    qs = [P.gen_queries(2, V, F, 3_000_000 + 200_000 * k, 150_000) for k in range(4)]
+    want = [eng.batch_query(q) for q in qs]
+    lib = L.cuda()
+    vp = lambda t: C.c_void_p(t.data_ptr())
+    errs = []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            n = len(qs[k])
+            dq = torch.from_numpy(qs[k]).cuda()
+            for _ in range(5):
+                od = torch.empty(n, dtype=torch.float64, device="cuda")
+                of, osi, ofl = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3))
+                oc = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+                torch.cuda.current_stream().synchronize()
+                L.check(lib.p2m_query_device(eng.handle, 0, vp(dq), n, vp(od), vp(oc), vp(of), vp(osi), vp(ofl),
+                                             C.c_void_p(st.cuda_stream), None))
+                st.synchronize()
+                assert od.cpu().numpy().tobytes() == want[k].distance.tobytes()
+                assert np.array_equal(of.cpu().numpy().view(np.uint32), want[k].face)
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
