@@ -242,7 +242,8 @@ struct p2m_engine {
     uint64_t bytes = 0;
     bool profiling = false;
     int scan_mode = P2M_SCAN_GROUPED;
-    int morton_bits = 24;  // P2M_MORTON_BITS (c2: 30 -> 24 bits saves a radix pass, scan unchanged)
+    int morton_bits = -1;  // P2M_MORTON_BITS; auto: 24 up to 16 M rows (c2: one radix pass fewer, scan
+                           // unchanged), 30 above (c5 at 100 M: the coarser order costs the scan more)
     int e2e_chunks = 0;  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
@@ -528,7 +529,8 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
     if (prof) CK(cudaEventRecord(ev[1], st));
     // the Morton order only has to be spatially coherent: sorting on the top morton_bits of the
     // 30-bit key saves radix passes (8 bits per onesweep pass)
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows, rows2, (int64_t)n, 30 - E->morton_bits, 30, st));
+    const int mbits = E->morton_bits > 0 ? E->morton_bits : (n > (16ull << 20) ? 30 : 24);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows, rows2, (int64_t)n, 30 - mbits, 30, st));
     if (prof) CK(cudaEventRecord(ev[2], st));
     if (nearest_only) {
         CK(p2m::dev::launch_nearest(s.params, d_q, rows2, n, d_site_only, st));

@@ -296,6 +296,9 @@ def test_host_api_chunk_schedules_identical(c2, chunks, monkeypatch):
     {"P2M_TILE_ORDER": "0"}, {"P2M_TILE_ORDER": "1"}, {"P2M_TILE_ORDER": "2"},  # launch orders
     {"P2M_MORTON_BITS": "30"}, {"P2M_MORTON_BITS": "9"},  # finer / much coarser Morton order
     {"P2M_LONG_TILE": "128"},                  # heavy-site tile height
+    {"P2M_HEAVY_E": "16"},                     # many more heavy sites (short tiles)
+    {"P2M_NO_SEED": "1"}, {"P2M_NO_BATCH": "1"},  # without the d_min seeds / group-sphere levels
+    {"P2M_NO_SPATIAL": "1"},                   # lists scanned in ascending face order
 ])
 def test_scan_schedules_identical(c2, env, monkeypatch):
     """The tile partition (CTA tiles vs one-warp small tiles), their launch order, the Morton
