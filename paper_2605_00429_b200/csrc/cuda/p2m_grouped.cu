@@ -37,6 +37,7 @@ namespace {
 
 constexpr int kTile = 256;
 
+
 #ifndef P2M_DESC_MINB
 #define P2M_DESC_MINB 5   // 48 registers, 5 CTAs/SM: the descent is load-latency bound (measured 0.77 -> 0.67 ms on c2)
 #endif
@@ -191,12 +192,11 @@ __device__ __forceinline__ float lb2_face(const float4* r, float qx, float qy, f
 // replica and R = 8 / G replicas; replica r scans the 32-candidate batches b == r (mod R) of every
 // staged chunk, so small groups still keep all 8 warps busy.  Per batch, each lane computes a
 // pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
-// warp walks the union of set bits in list order; a lane whose bit is set applies the oracle's fp64
-// sphere test with its CURRENT d_min and, on pass, the exact point-triangle kernel on the triangle
-// staged in shared memory (all lanes read the same record: broadcast).  Because the pre-filter can
-// only skip candidates the fp64 test would skip, each replica evaluates exactly the candidates the
-// sequential oracle would (so with R = 1 the counters match the oracle too).  Replicas are merged by
-// the lexicographic min of (d^2, face id), the sequential argmin.
+// warp walks the union of set bits in list order; a lane whose bit is set applies the tight fp32
+// lower bound with its CURRENT d_min and, on pass, the exact point-triangle kernel on the face
+// record (all lanes read the same record: broadcast).  Every prune is conservative (DESIGN.md
+// section 9), so each row's result is the full-list argmin.  Replicas are merged by the
+// lexicographic min of (d^2, face id), the sequential argmin.
 constexpr int kChunk = 256;
 constexpr int kWinChunks = 256;                  // level-0 need bits are computed per window of chunks
 static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
@@ -206,13 +206,14 @@ constexpr int kWarps = kTile / 32;
 // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)}, lb: 32 x
 // 64-byte lower-bound records, fid: 32 face ids), scanned for this lane's row.  Each lane computes a
 // pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
-// warp walks the union of set bits in list order; a lane whose bit is set re-tests with its CURRENT
-// d_min, applies the tight fp32 lower bound, and survivors run the exact fp64 kernel on the face
-// record (all lanes read the same record: broadcast).  stage_lb: the lower-bound records of the
+// warp walks the union of set bits in list order; a lane whose bit is set applies the tight fp32
+// lower bound with its CURRENT d_min, and survivors run the exact fp64 kernel on the face record
+// (all lanes read the same record: broadcast).  (Re-testing the fp32 sphere first was measured
+// slower: the lower bound subsumes it.)  stage_lb: the lower-bound records of the
 // union are loaded here (lane k holds entry k's face id my_f).  Called by every lane of the warp.
 template <bool kCounters>
 __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, const V& q, uint64_t QX, uint64_t QY,
-                                               uint64_t QZ, uint64_t& DK, double& best, double& dmin, uint32_t& bf,
+                                               uint64_t QZ, uint64_t& DK, double& best, uint32_t& bf,
                                                uint32_t& exact, unsigned long long& passes,
                                                unsigned long long& rare_iters, const float4* pair, float4* lb,
                                                const uint32_t* fid, int valid, bool stage_lb, uint32_t my_f,
@@ -255,21 +256,12 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         }
         __syncwarp();
     }
-    const float* pf = reinterpret_cast<const float*>(pair);
-    // the exact test of one candidate kk of this lane, after re-testing with the CURRENT d_min
-    // (the batch mask used the d_min of the batch start): the same conservative fp32 sphere
-    // test, then the tight lower bound, then fp64
+    // the exact test of one candidate kk of this lane: the tight lower bound against the CURRENT
+    // d_min (the batch mask used the d_min of the batch start), then fp64
     auto visit = [&](int kk) {
         {
-            const int pp = kk >> 1, h = kk & 1;
             float dkx, dky;
             upk2(DK, dkx, dky);
-            const float dx = qxf - pf[8 * pp + h];
-            const float dy = qyf - pf[8 * pp + 2 + h];
-            const float dz = qzf - pf[8 * pp + 4 + h];
-            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            const float th = __fadd_ru(pf[8 * pp + 6 + h], dkx);
-            if (d2f > __fmul_ru(th, th)) return;
             const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
             if (lb2_face(lb + 4 * kk, qxf, qyf, qzf) > __fmul_ru(thl, thl)) return;
         }
@@ -281,8 +273,9 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         if (dd < best || (dd == best && f < bf)) {
             best = dd;
             bf = f;
-            dmin = sqrt(dd);
-            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+            // any upper bound of sqrt(best) is a valid d_min for the prunes: the fp32 sqrt rounded up of
+            // best rounded up (cheaper than the fp64 sqrt)
+            const float dkf = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(dd)), delta), K);
             DK = pk2(dkf, dkf);
         }
     };
@@ -471,7 +464,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                 wpf[8 * pp + 6 + h] = rv.w;
             }
             __syncwarp();
-            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, dmin, bf, exact, passes, rare_iters, wp,
+            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, wp,
                                       wl, wf, valid, true, f, lane);
             __syncwarp();                        // the slice is rewritten by the next batch
         }
@@ -666,13 +659,13 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)},
         // lb: 32 x 64-byte lower-bound records, fid: 32 face ids).  Each lane computes a pass/prune bit
         // per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the warp
-        // walks the union of set bits in list order; a lane whose bit is set re-tests with its
-        // CURRENT d_min, applies the tight fp32 lower bound, and survivors run the exact fp64 kernel
-        // on the face record (all lanes read the same record: broadcast).  stage_lb: the lower-bound
+        // walks the union of set bits in list order; a lane whose bit is set applies the tight fp32
+        // lower bound with its CURRENT d_min, and survivors run the exact fp64 kernel on the face
+        // record (all lanes read the same record: broadcast).  stage_lb: the lower-bound
         // records of the union are loaded here (lane k holds entry k's face id my_f).
         auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
                               uint32_t my_f) {
-            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, dmin, bf, exact, passes, rare_iters, pair,
+            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, pair,
                                       lb, fid, valid, stage_lb, my_f, lane);
         };
         if (G == 1) {
