@@ -811,8 +811,10 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             for (int pos = r; pos < nb; pos += R) {
                 const int bb = P2M_BATCH_ORDER ? (int)s_bord[pos] : pos;
                 // pruned whole by its batch sphere for every row (cneed: the union over the replicas'
-                // level-1 votes -- with the reordering a replica scans batches another one voted on)
-                if (!((cneed >> bb) & 1u)) continue;
+                // level-1 votes -- with the reordering a replica scans batches another one voted on).
+                // Without replicas each warp voted on every batch for its own rows: a batch its own
+                // vote pruned stays pruned (d_min only shrinks), so it is skipped too.
+                if (!(((R == 1 ? wneed : cneed) >> bb) & 1u)) continue;
                 const int k0 = bb * 32;
                 scan_batch(s_pair + k0, s_lb + 4 * k0, s_fid + k0, mc - k0, false, 0u);
             }
