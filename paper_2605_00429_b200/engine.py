@@ -151,7 +151,10 @@ class HostEngine:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            L.host().p2m_host_engine_destroy(h)
+            try:
+                L.host().p2m_host_engine_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     @property
@@ -253,7 +256,10 @@ class Engine:
     def close(self):
         h = getattr(self, "_h", None)
         if h:
-            L.cuda().p2m_engine_destroy(h)
+            try:
+                L.cuda().p2m_engine_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     __del__ = close
