@@ -506,6 +506,9 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
 }
 
 
+#ifndef P2M_EARLY1
+#define P2M_EARLY1 1  // single-chunk CTA tiles: chunk loads issued before the seeds (cp.async for the spheres)
+#endif
 #ifndef P2M_BATCH_ORDER
 #define P2M_BATCH_ORDER 1   // block path: visit a chunk's batches best-first for the tile's first row
 #endif
@@ -574,12 +577,25 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
 #define qxf __uint_as_float((uint32_t)QX)
 #define qyf __uint_as_float((uint32_t)QY)
 #define qzf __uint_as_float((uint32_t)QZ)
-    if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
     // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
     uint32_t nf = 0;
     float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
     uint32_t pre_c = 0xffffffffu;                // chunk held in (nf, nv)
     bool first_chunk = true;
+#if P2M_EARLY1
+    const bool early = nch == 1 && G > 1;        // the one chunk of a single-chunk CTA tile: its loads
+    if (early) {                                 // start now and land during the seed computation
+        const int mc0 = (int)min((uint64_t)kChunk, end - beg);
+        if (tid < ((mc0 + 31) >> 5)) {           // batch spheres: async copy to shared, no registers
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_bsph[tid]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(p.bsph + bo + tid));
+            asm volatile("cp.async.commit_group;");
+        }
+        if (tid < mc0) { nf = p.lfs[beg + tid]; nv = p.f32[nf]; }
+        pre_c = 0;
+    }
+#endif
+    if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
     for (uint32_t w0 = 0; w0 < nch; w0 += kWinChunks) {
         const uint32_t wn = min(nch - w0, (uint32_t)kWinChunks);
         const int nwords = (int)((wn + 31) >> 5);
@@ -733,7 +749,15 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             // level 1: the enclosing sphere of each 32-entry batch.  If every lane's conservative fp32
             // bound to it exceeds the lane's d_min, every member sphere's bound does too, so the whole
             // batch is pruned exactly as the per-candidate tests would prune it (and is never staged).
+#if P2M_EARLY1
+            if (early) {
+                if (tid < nb) asm volatile("cp.async.wait_all;" ::: "memory");
+            } else if (tid < nb) {
+                s_bsph[tid] = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + tid];
+            }
+#else
             if (tid < nb) s_bsph[tid] = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + tid];
+#endif
             if (tid == 0) s_need = 0u;
             __syncthreads();
             uint32_t wneed = 0;
