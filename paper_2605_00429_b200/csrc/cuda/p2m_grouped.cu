@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
 
 
 #ifndef P2M_EARLY1
-#define P2M_EARLY1 1  // single-chunk CTA tiles: chunk loads issued before the seeds (cp.async for the spheres)
+#define P2M_EARLY1 2  // single-chunk CTA tiles: chunk loads issued before the seeds (cp.async spheres; 2: + records)
 #endif
 #ifndef P2M_BATCH_ORDER
 #define P2M_BATCH_ORDER 1   // block path: visit a chunk's batches best-first for the tile's first row
@@ -596,6 +596,18 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     }
 #endif
     if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
+#if P2M_EARLY1 >= 2
+    if (early && tid < (int)min((uint64_t)kChunk, end - beg)) {
+        // the chunk's lower-bound records, async into shared memory (nf has landed by now); waited
+        // for just before the staging barrier
+        const float4* lr = p.lbr + 4 * (uint64_t)nf;
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_lb[4 * tid]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa + 16 * k), "l"(lr + k));
+    }
+    asm volatile("cp.async.commit_group;");
+#endif
     for (uint32_t w0 = 0; w0 < nch; w0 += kWinChunks) {
         const uint32_t wn = min(nch - w0, (uint32_t)kWinChunks);
         const int nwords = (int)((wn + 31) >> 5);
@@ -751,7 +763,11 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             // batch is pruned exactly as the per-candidate tests would prune it (and is never staged).
 #if P2M_EARLY1
             if (early) {
+#if P2M_EARLY1 >= 2
+                if (tid < nb) asm volatile("cp.async.wait_group 1;" ::: "memory");  // spheres, not the records
+#else
                 if (tid < nb) asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
             } else if (tid < nb) {
                 s_bsph[tid] = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + tid];
             }
@@ -817,6 +833,10 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 const int pp = tid >> 1, h = tid & 1;
                 if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
                 s_fid[tid] = nf;
+#if P2M_EARLY1 >= 2
+                if (early) asm volatile("cp.async.wait_all;" ::: "memory");  // records copied at tile start
+                else
+#endif
                 if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the lower-bound record (rare path, broadcast)
                     const float4* lr = p.lbr + 4 * (uint64_t)nf;
                     s_lb[4 * tid] = lr[0];
