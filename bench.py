@@ -382,6 +382,10 @@ def main():
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_scan_tiles (site-tiled pruned list scan, exact fp64)",
+                     # the DRAM bytes ncu measured for this kernel (traffic) over the live kernel time:
+                     # the structure is L2/SMEM-resident, so real HBM use is a small fraction of peak
+                     "measured_dram_gbs": (traffic / t_scan_s / 1e9) if traffic else None,
+                     "measured_dram_frac": (traffic / t_scan_s / 1e9 / peak) if traffic else None,
                      "algorithmic_bytes_per_launch": B_scan,
                      "bytes_per_query": "72 + 36 C_q + 72 E_q (SURVEY.md 8(d) minus the 32 n_q of the descent kernel)",
                      "pipeline_algorithmic_gbs": pipeline_gbs, "pipeline_bytes_per_step": B_alg,
