@@ -244,7 +244,8 @@ struct p2m_engine {
     int scan_mode = P2M_SCAN_GROUPED;
     int morton_bits = -1;  // P2M_MORTON_BITS; auto: 24 up to 16 M rows (c2: one radix pass fewer, scan
                            // unchanged), 30 above (c5 at 100 M: the coarser order costs the scan more)
-    int e2e_chunks = 0;  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
+    int e2e_chunks = 0;
+    double e2e_sched[4] = {1.0 / 32, 2.0, 0.25, 0.0};  // first, growth, cap, tail (P2M_E2E_SCHED)  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
     uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
@@ -1005,6 +1006,12 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         s->params.adj = s->adj;
     }
     if (const char* v = std::getenv("P2M_MORTON_BITS")) E->morton_bits = std::min(30, std::max(3, std::atoi(v)));
+    if (const char* v = std::getenv("P2M_E2E_SCHED")) {
+        double x[4];
+        if (std::sscanf(v, "%lf,%lf,%lf,%lf", &x[0], &x[1], &x[2], &x[3]) == 4 && x[0] > 0 && x[1] >= 1 && x[2] > 0 &&
+            x[3] >= 0 && x[3] < 1)
+            for (int k = 0; k < 4; ++k) E->e2e_sched[k] = x[k];
+    }
     if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(0, std::atoi(v));
     {
         int rc = mark_heavy_sites(E.get(), d);
@@ -1122,14 +1129,20 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
                 const uint64_t c0 = std::max<uint64_t>(1ull << 16, (m + k - 1) / k);
                 for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
             } else {
-                const uint64_t cmax = std::max<uint64_t>(1ull << 18, (m + 3) / 4);
-                uint64_t cur = std::min(cmax, std::max<uint64_t>(1ull << 18, m / 32));
-                for (uint64_t off = 0; off < m;) {
-                    const uint64_t l = std::min(cur, m - off);
+                // geometric: first chunk m*first, growing by `growth` up to m*cap, the last m*tail rows
+                // as a separate small chunk (its D2H is the pipeline's drain)
+                const double first = e->e2e_sched[0], growth = e->e2e_sched[1], cap = e->e2e_sched[2],
+                             tail = e->e2e_sched[3];
+                const uint64_t cmax = std::max<uint64_t>(1ull << 18, (uint64_t)(cap * (double)m));
+                const uint64_t mt = std::min<uint64_t>(m, (uint64_t)(tail * (double)m));
+                uint64_t cur = std::min(cmax, std::max<uint64_t>(1ull << 18, (uint64_t)(first * (double)m)));
+                for (uint64_t off = 0; off < m - mt;) {
+                    const uint64_t l = std::min(cur, m - mt - off);
                     len_of.push_back(l);
                     off += l;
-                    cur = std::min(cmax, 2 * cur);
+                    cur = std::min(cmax, (uint64_t)(growth * (double)cur));
                 }
+                if (mt) len_of.push_back(mt);
             }
             if (len_of.size() > (size_t)Slot::kMaxChunks) {  // fold the tail into equal chunks
                 const uint64_t c0 = (m + Slot::kMaxChunks - 1) / Slot::kMaxChunks;
