@@ -357,3 +357,15 @@ def test_concurrent_device_calls_one_engine(c2):
     for t in th:
         t.join()
     assert not errs, errs
+
+
+@pytest.mark.parametrize("sched", ["0.05,3,0.4,0.1", "0.3,1,0.3,0.05"])
+def test_host_api_geometric_schedules_identical(c2, sched, monkeypatch):
+    """The geometric host-API schedule (first, growth, cap, tail) never changes a row."""
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 1_500_000, 900_000)
+    base = P.Engine(h).batch_query(q)
+    monkeypatch.setenv("P2M_E2E_SCHED", sched)
+    r = P.Engine(h).batch_query(q)
+    _compare(r, {"site": base.site, "face": base.face, "flags": base.flags, "distance": base.distance,
+                 "closest": base.closest}, len(q))
