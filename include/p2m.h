@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define P2M_ABI_VERSION 1
+#define P2M_ABI_VERSION 2
 
 /* ---- status codes (GeometryError REF/proj/include/p2mx/geom.hpp:88-91 -> P2M_ERR_GEOMETRY) ---- */
 enum {
@@ -46,7 +46,12 @@ enum { P2M_SITE_MESH_VERTEX = 0, P2M_SITE_SENTINEL = 1, P2M_SITE_AUXILIARY = 2 }
 /* ---- per-query flags (QueryResult fallback flag, REF/SPEC.md:468,491,611) ---- */
 enum {
     P2M_FLAG_FALLBACK = 1u,      /* answered by the exact BVH closest-point search, not a table */
-    P2M_FLAG_OUT_OF_DOMAIN = 2u  /* q outside D (REF/SPEC.md:648) */
+    P2M_FLAG_OUT_OF_DOMAIN = 2u, /* q outside D (REF/SPEC.md:648) */
+    P2M_FLAG_TABLE_MISS = 4u     /* the nearest site's list had no face within the distance bound
+                                    |q - ref(site)| -- the table is not a superset of the faces that
+                                    can be nearest in the site's cell (REF/SPEC.md:435 violated, e.g.
+                                    a hand-filled p2m_engine_desc); the row is answered exactly by
+                                    the BVH fallback and also carries P2M_FLAG_FALLBACK */
 };
 
 /* Thread-local description of the last failure on this thread ("" if none). */
@@ -92,6 +97,11 @@ typedef struct p2m_counters {
     uint64_t kd_nodes_visited;   /* nearest-site candidates evaluated (k-d nodes or grid candidates) */
     uint64_t filter_passes;      /* grouped scan: candidates passing the first fp32 sphere test (diag.) */
     uint64_t warp_rare_iters;    /* grouped scan: warp-level rare-path iterations x 32 (diagnostic) */
+    uint64_t structure_bytes;    /* grouped scan: bytes of the read-only structure the scan kernels load,
+                                    each staged list chunk counted once per tile, each face record once
+                                    per warp visit (the roofline's algorithmic bytes, with 64 B per row
+                                    of q/row index in and results out) -- ABI v2 */
+    uint64_t scan_tiles;         /* grouped scan: tiles scanned (CTA tiles + one-warp tiles) -- ABI v2 */
 } p2m_counters;
 
 typedef struct p2m_engine p2m_engine;

@@ -23,7 +23,7 @@ ERRORS = {
     -7: "P2M_ERR_INTERNAL",
 }
 SITE_MESH_VERTEX, SITE_SENTINEL, SITE_AUXILIARY = 0, 1, 2
-FLAG_FALLBACK, FLAG_OUT_OF_DOMAIN = 1, 2
+FLAG_FALLBACK, FLAG_OUT_OF_DOMAIN, FLAG_TABLE_MISS = 1, 2, 4
 
 dp = C.POINTER(C.c_double)
 u8p = C.POINTER(C.c_uint8)
@@ -60,6 +60,8 @@ class Counters(C.Structure):
         ("kd_nodes_visited", C.c_uint64),
         ("filter_passes", C.c_uint64),
         ("warp_rare_iters", C.c_uint64),
+        ("structure_bytes", C.c_uint64),
+        ("scan_tiles", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -79,6 +79,7 @@ __device__ __forceinline__ void load_tri(const D4* rec, V* a, V* b, V* c) {
     *c = V{t1.z, t1.w, t2.x};
 }
 
+constexpr int kLbRec = 6;   // float4 per fp32 lower-bound record (p2m_grouped.cu lb2_face)
 constexpr uint64_t kIdMask = 0xffffffffull;
 constexpr int kDimShift = 32;
 constexpr uint64_t kSentinelBit = 1ull << 34;
@@ -88,8 +89,8 @@ struct Params {
     uint32_t n_nodes;
     const D4* rec;          // 4 per face
     const float4* f32;      // per face fp32 pre-filter record: c rounded to nearest, r_up * K rounded up
-    const float4* lbr;      // per face 4 x float4: a, unit normal n, in-plane outward edge normals m_ab,
-                            // m_bc, m_ca, offset m_bc.(b-a) -- the tight lower bound sqrt(h^2+max(0,s_i)^2)
+    const float4* lbr;      // per face kLbRec = 6 x float4: a, unit normal n, in-plane outward edge normals
+                            // m_ab, m_bc, m_ca, offset m_bc.(b-a), b, c -- the tight lower bound (lb2_face)
     float lb_margin;        // absolute fp32 error bound of that lower bound (64 * 2^-24 * M)
     const uint64_t* off;    // S+1
     const uint64_t* boff;   // S+1: first batch sphere of each list (one per aligned 32 entries of lfs)

@@ -9,11 +9,13 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -33,6 +35,7 @@ extern "C" void p2m_set_last_error_internal(const char* msg);  // libp2m_host.so
 
 using p2m::dev::D4;
 using p2m::dev::Params;
+using p2m::dev::kLbRec;
 
 namespace {
 
@@ -169,6 +172,65 @@ void build_bvh(const double* tri, uint64_t nf, FlatBvh& out) {
     rec.go(0, (uint32_t)nf);
 }
 
+// Host copy pool of the pageable-buffer path: a few persistent threads that split a list of memcpy
+// segments into 2 MB pieces (one core's memcpy runs well below the host's memory bandwidth, and
+// spawning threads per sub-chunk would cost more than the copy).  run() blocks; the caller works too.
+class CopyPool {
+  public:
+    struct Seg { void* dst; const void* src; size_t bytes; };
+    explicit CopyPool(int n) {
+        for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~CopyPool() {
+        { std::lock_guard<std::mutex> lk(mu_); stop_ = true; }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void run(const Seg* segs, int nseg) {
+        pieces_.clear();
+        const size_t kPiece = 2u << 20;
+        for (int i = 0; i < nseg; ++i)
+            for (size_t o = 0; o < segs[i].bytes; o += kPiece)
+                pieces_.push_back(Seg{(char*)segs[i].dst + o, (const char*)segs[i].src + o, std::min(kPiece, segs[i].bytes - o)});
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            next_.store(0);
+            busy_ = (int)th_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return busy_ == 0; });
+    }
+  private:
+    void work() {
+        for (size_t i; (i = next_.fetch_add(1)) < pieces_.size();) std::memcpy(pieces_[i].dst, pieces_[i].src, pieces_[i].bytes);
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--busy_ == 0) done_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::vector<Seg> pieces_;
+    std::atomic<size_t> next_{0};
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    uint64_t gen_ = 0;
+    int busy_ = 0;
+    bool stop_ = false;
+};
+
 // Per-call working set of run_pipeline (keys/rows double buffers, CUB temp, tile arrays).
 struct Scratch {
     uint32_t *keys = nullptr, *rows = nullptr, *keys2 = nullptr, *rows2 = nullptr;
@@ -225,6 +287,19 @@ struct Slot {
                      // wait on each other through the stream-ordered allocator's reuse dependencies
     } ws[kPipe];
     uint64_t cap = 0;
+    // pageable host buffers (p2m_query): pinned bounce rings, sub-chunks of kRows rows.  The calling
+    // thread packs input sub-chunks into the in-ring (host memcpy) and enqueues their H2D copies; a
+    // second thread enqueues the D2H copies of finished chunks into the out-ring and unpacks them into
+    // the caller's arrays, so both host copies overlap the kernels and the PCIe transfers.
+    struct Bounce {
+        static constexpr uint64_t kRows = 1ull << 20;
+        static constexpr int kIn = 3, kOut = 4;
+        double* in[kIn] = {};
+        unsigned char* out[kOut] = {};   // dist 8 | cp 24 | face 4 | site 4 | flags 4 per row, as 5 arrays
+        cudaEvent_t in_ev[kIn] = {}, out_ev[kOut] = {};
+        std::unique_ptr<CopyPool> pack, unpack;  // host copy threads of the two directions
+        bool ready = false;
+    } bnc;
     cudaEvent_t agg_ready = nullptr;
     unsigned long long* agg = nullptr;
     // profiling: ring of event sets, read lazily by p2m_last_timings (no host sync per call)
@@ -281,6 +356,10 @@ void free_slot(Slot& s) {
     s.cev.clear();
     if (s.t0) cudaEventDestroy(s.t0);
     if (s.agg_ready) cudaEventDestroy(s.agg_ready);
+    for (auto& b : s.bnc.in) if (b) cudaFreeHost(b);
+    for (auto& b : s.bnc.out) if (b) cudaFreeHost(b);
+    for (auto& e : s.bnc.in_ev) if (e) cudaEventDestroy(e);
+    for (auto& e : s.bnc.out_ev) if (e) cudaEventDestroy(e);
     cudaFree(s.agg);
     for (auto& e : s.ev) if (e) cudaEventDestroy(e);
     s.ev.clear();
@@ -402,7 +481,7 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.bsph, sizeof(float4) * std::max<uint64_t>(1, E.n_batches)));
-    CK(cudaMalloc(&s.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.lbr, sizeof(float4) * kLbRec * std::max<uint64_t>(1, E.n_faces)));
     CK(cudaMalloc(&s.boff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
@@ -565,8 +644,12 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         {
             std::unique_lock<std::mutex> lk(s.side_mu, std::defer_lock);
             if (side == Slot::kPipe) lk.lock();  // host-API pipes run under the slot mutex already
+            p2m::dev::Out om = o;
+            om.miss = tix;                       // free after tile construction: the table-miss queue
+            om.miss_n = meta + 3;
             CK(p2m::dev::launch_scan_tiles(prm, d_q, rows, keys2, tiles, meta, tord ? tord + 3 * max_t : nullptr, n,
-                                           o, counters, st, s.side[side], s.fork[side], s.join[side]));
+                                           om, counters, st, s.side[side], s.fork[side], s.join[side]));
+            CK(p2m::dev::launch_table_miss(prm, d_q, om, st));
         }
         if (trace) {
             std::vector<unsigned long long> h(4 * ntile_max);
@@ -809,9 +892,10 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
                 csph[ci] = group_sphere(j, std::min(b1, j + kListChunk));
         }
     });
-    // tight fp32 lower-bound records (k_scan_tiles rare path): d(q,T)^2 >= h^2 + max(0, s_i)^2 with
-    // h = n.(q-a) and s_i the signed in-plane distances to the three edge lines (outward positive)
-    std::vector<float4> lbr(4 * std::max<uint64_t>(1, F));
+    // tight fp32 lower-bound records (the scan's rare path, p2m_grouped.cu lb2_face): d(q,T)^2 >=
+    // h^2 + max(0, s_i)^2 with h = n.(q-a) and s_i the signed in-plane distances to the three edge
+    // lines (outward positive), and the support bound along q - V for the nearest vertex V (b, c)
+    std::vector<float4> lbr(kLbRec * std::max<uint64_t>(1, F));
     for (uint64_t f = 0; f < F; ++f) {
         const double* t = d->tri_xyz + 9 * f;
         const double A[3] = {t[0], t[1], t[2]}, B[3] = {t[3], t[4], t[5]}, Cc[3] = {t[6], t[7], t[8]};
@@ -833,10 +917,13 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         ok = ok && unit(m1) && unit(m2) && unit(m3);
         if (!ok) { for (int k = 0; k < 3; ++k) n[k] = m1[k] = m2[k] = m3[k] = 0.0; }  // never prunes
         const double o2 = ok ? (m2[0] * ab[0] + m2[1] * ab[1] + m2[2] * ab[2]) : 0.0;
-        lbr[4 * f] = make_float4((float)A[0], (float)A[1], (float)A[2], (float)n[0]);
-        lbr[4 * f + 1] = make_float4((float)n[1], (float)n[2], (float)m1[0], (float)m1[1]);
-        lbr[4 * f + 2] = make_float4((float)m1[2], (float)m2[0], (float)m2[1], (float)m2[2]);
-        lbr[4 * f + 3] = make_float4((float)m3[0], (float)m3[1], (float)m3[2], (float)o2);
+        float4* L = lbr.data() + kLbRec * f;
+        L[0] = make_float4((float)A[0], (float)A[1], (float)A[2], (float)n[0]);
+        L[1] = make_float4((float)n[1], (float)n[2], (float)m1[0], (float)m1[1]);
+        L[2] = make_float4((float)m1[2], (float)m2[0], (float)m2[1], (float)m2[2]);
+        L[3] = make_float4((float)m3[0], (float)m3[1], (float)m3[2], (float)o2);
+        L[4] = make_float4((float)B[0], (float)B[1], (float)B[2], (float)Cc[0]);
+        L[5] = make_float4((float)Cc[1], (float)Cc[2], 0.f, 0.f);
     }
     FlatBvh bvh;
     build_bvh(d->tri_xyz, F, bvh);
@@ -968,7 +1055,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         struct { void* dst; const void* src; size_t n; } cp[] = {
             {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
             {s.bsph, s0.bsph, sizeof(float4) * std::max<uint64_t>(1, E->n_batches)}, {s.boff, s0.boff, 8 * (S + 1)},
-            {s.lbr, s0.lbr, sizeof(float4) * 4 * std::max<uint64_t>(1, F)},
+            {s.lbr, s0.lbr, sizeof(float4) * kLbRec * std::max<uint64_t>(1, F)},
             {s.off, s0.off, 8 * (S + 1)},
             {s.lf, s0.lf, 4 * L}, {s.lfs, s0.lfs, 4 * L},
             {s.csph, s0.csph, sizeof(float4) * std::max<uint64_t>(1, E->n_chunks)}, {s.coff, s0.coff, 8 * (S + 1)},
@@ -1065,6 +1152,8 @@ P2M_API int p2m_query_device(p2m_engine* e, int slot, const double* d_q, uint64_
         cnt->kd_nodes_visited = h[2];
         cnt->filter_passes = h[4];
         cnt->warp_rare_iters = h[5];
+        cnt->structure_bytes = h[6];
+        cnt->scan_tiles = h[7];
         cnt->fallbacks = h[3];
     }
     return P2M_OK;
@@ -1095,6 +1184,171 @@ P2M_API int p2m_query_device_counters(p2m_engine* e, int slot, const double* d_q
     int rc = run_pipeline(e, s, d_q, n, o, true, st, false, nullptr);
     cudaFreeAsync(dist, st); cudaFreeAsync(cp, st); cudaFreeAsync(face, st); cudaFreeAsync(site, st);
     return rc;
+}
+
+// true if the host pointer is page-locked (cudaHostAlloc / cudaHostRegister) -- the DMA engines can
+// read or write it asynchronously; pageable memory goes through the bounce rings
+bool host_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int ensure_bounce(Slot& s) {
+    auto& b = s.bnc;
+    if (b.ready) return P2M_OK;
+    for (int k = 0; k < Slot::Bounce::kIn; ++k) {
+        CK(cudaHostAlloc((void**)&b.in[k], 24 * Slot::Bounce::kRows, cudaHostAllocPortable));
+        CK(cudaEventCreateWithFlags(&b.in_ev[k], cudaEventDisableTiming));
+    }
+    for (int k = 0; k < Slot::Bounce::kOut; ++k) {
+        CK(cudaHostAlloc((void**)&b.out[k], 44 * Slot::Bounce::kRows, cudaHostAllocPortable));
+        CK(cudaEventCreateWithFlags(&b.out_ev[k], cudaEventDisableTiming));
+    }
+    const int hw = (int)std::max(2u, std::thread::hardware_concurrency());
+    b.pack.reset(new CopyPool(std::min(3, hw / 4)));
+    b.unpack.reset(new CopyPool(std::min(5, hw / 3)));
+    b.ready = true;
+    return P2M_OK;
+}
+
+// The host-buffer pipeline for pageable caller arrays (p2m_query): the same chunk schedule, device
+// staging sets and streams as the pinned path; every H2D/D2H copy goes through a pinned bounce
+// sub-chunk.  This thread: pack input sub-chunks + enqueue H2D, then the chunk's kernels.  Output
+// thread: per finished chunk, enqueue D2H sub-copies into the out-ring, unpack completed ones.
+int run_bounce(p2m_engine* e, Slot& s, const double* q, double* dist, double* cp, uint32_t* face, uint32_t* site,
+               uint32_t* flags, uint64_t b, const std::vector<uint64_t>& len_of, p2m_counters* cnt,
+               p2m_counters& part) {
+    using B = Slot::Bounce;
+    auto& bn = s.bnc;
+    const size_t nch = len_of.size();
+    std::vector<uint64_t> start(nch);
+    for (size_t c = 0, o = 0; c < nch; ++c) { start[c] = o; o += len_of[c]; }
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t launched = 0, drained = 0;  // chunks whose kernels are enqueued / whose D2H copies are enqueued
+    int out_rc = P2M_OK;
+    std::string out_err;
+    std::thread out([&] {
+        int rc = P2M_OK;
+        auto fail = [&](int r) { rc = r; out_err = p2m_last_error(); };
+        if (cudaSetDevice(s.dev) != cudaSuccess) { set_err("cudaSetDevice"); fail(P2M_ERR_CUDA); }
+        struct Pend { uint64_t r0 = 0, len = 0; bool live = false; } pend[B::kOut];
+        auto unpack = [&](int k) {
+            Pend& p = pend[k];
+            if (!p.live) return (int)P2M_OK;
+            if (cudaEventSynchronize(bn.out_ev[k]) != cudaSuccess) { set_err("bounce D2H failed"); return (int)P2M_ERR_CUDA; }
+            const unsigned char* o = bn.out[k];
+            const uint64_t L = p.len, r = b + p.r0;
+            const CopyPool::Seg segs[5] = {{dist + r, o, 8 * L}, {cp + 3 * r, o + 8 * B::kRows, 24 * L},
+                                           {face + r, o + 32 * B::kRows, 4 * L}, {site + r, o + 36 * B::kRows, 4 * L},
+                                           {flags ? flags + r : nullptr, o + 40 * B::kRows, flags ? 4 * L : 0}};
+            bn.unpack->run(segs, 5);
+            p.live = false;
+            return (int)P2M_OK;
+        };
+        uint64_t j = 0;
+        for (size_t c = 0; c < nch && rc == P2M_OK; ++c) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return launched > c || out_rc != P2M_OK; });
+                if (out_rc != P2M_OK) break;
+            }
+            const Slot::Ws& w = s.ws[c % Slot::kPipe];
+            if (cudaStreamWaitEvent(s.d2h, s.cev[3 * c + 1], 0) != cudaSuccess) { set_err("d2h wait"); fail(P2M_ERR_CUDA); break; }
+            for (uint64_t o = 0; o < len_of[c] && rc == P2M_OK; o += B::kRows, ++j) {
+                const int k = (int)(j % B::kOut);
+                int r2 = unpack(k);
+                if (r2 != P2M_OK) { fail(r2); break; }
+                const uint64_t L = std::min(B::kRows, len_of[c] - o);
+                unsigned char* ob = bn.out[k];
+                cudaError_t ce = cudaSuccess;
+                ce = cudaMemcpyAsync(ob, w.dist + o, 8 * L, cudaMemcpyDeviceToHost, s.d2h);
+                if (ce == cudaSuccess) ce = cudaMemcpyAsync(ob + 8 * B::kRows, w.cp + 3 * o, 24 * L, cudaMemcpyDeviceToHost, s.d2h);
+                if (ce == cudaSuccess) ce = cudaMemcpyAsync(ob + 32 * B::kRows, w.face + o, 4 * L, cudaMemcpyDeviceToHost, s.d2h);
+                if (ce == cudaSuccess) ce = cudaMemcpyAsync(ob + 36 * B::kRows, w.site + o, 4 * L, cudaMemcpyDeviceToHost, s.d2h);
+                if (ce == cudaSuccess && flags) ce = cudaMemcpyAsync(ob + 40 * B::kRows, w.flags + o, 4 * L, cudaMemcpyDeviceToHost, s.d2h);
+                if (ce == cudaSuccess) ce = cudaEventRecord(bn.out_ev[k], s.d2h);
+                if (ce != cudaSuccess) { set_err(std::string("bounce D2H: ") + cudaGetErrorString(ce)); fail(P2M_ERR_CUDA); break; }
+                pend[k] = Pend{start[c] + o, L, true};
+            }
+            if (rc == P2M_OK && cudaEventRecord(s.cev[3 * c + 2], s.d2h) != cudaSuccess) { set_err("d2h record"); fail(P2M_ERR_CUDA); }
+            std::lock_guard<std::mutex> lk(mu);
+            drained = c + 1;
+            cv.notify_all();
+        }
+        for (int k = 0; k < B::kOut && rc == P2M_OK; ++k) {
+            int r2 = unpack((int)((j + k) % B::kOut));
+            if (r2 != P2M_OK) fail(r2);
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        if (rc != P2M_OK) out_rc = rc;
+        drained = nch;
+        cv.notify_all();
+    });
+    int rc = P2M_OK;
+    uint64_t i = 0;
+    for (size_t c = 0; c < nch && rc == P2M_OK; ++c) {
+        const uint64_t len = len_of[c];
+        const int k = (int)(c % Slot::kPipe);
+        cudaStream_t st = s.pipe[k];
+        Slot::Ws& w = s.ws[k];
+        if (c >= (size_t)Slot::kPipe) {
+            // staging set k is reused: its previous chunk's D2H copies must be enqueued (host side)
+            // before this chunk's H2D may be ordered after them
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return drained >= c - Slot::kPipe + 1 || out_rc != P2M_OK; });
+            if (out_rc != P2M_OK) break;
+            lk.unlock();
+            if (cudaStreamWaitEvent(s.h2d, s.cev[3 * (c - Slot::kPipe) + 1], 0) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
+        }
+        for (uint64_t o = 0; o < len; o += B::kRows, ++i) {
+            const int kk = (int)(i % B::kIn);
+            if (i >= (uint64_t)B::kIn && cudaEventSynchronize(bn.in_ev[kk]) != cudaSuccess) { set_err("bounce H2D failed"); rc = P2M_ERR_CUDA; break; }
+            const uint64_t L = std::min(B::kRows, len - o);
+            const CopyPool::Seg seg{bn.in[kk], q + 3 * (b + start[c] + o), 24 * L};
+            bn.pack->run(&seg, 1);
+            if (cudaMemcpyAsync(w.q + 3 * o, bn.in[kk], 24 * L, cudaMemcpyHostToDevice, s.h2d) != cudaSuccess ||
+                cudaEventRecord(bn.in_ev[kk], s.h2d) != cudaSuccess) { set_err("bounce H2D enqueue failed"); rc = P2M_ERR_CUDA; break; }
+        }
+        if (rc != P2M_OK) break;
+        cudaEvent_t ev_in = s.cev[3 * c], ev_k = s.cev[3 * c + 1];
+        if (cudaEventRecord(ev_in, s.h2d) != cudaSuccess || cudaStreamWaitEvent(st, ev_in, 0) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
+        if (c >= (size_t)Slot::kPipe && cudaStreamWaitEvent(st, s.cev[3 * (c - Slot::kPipe) + 2], 0) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
+        p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
+        rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false, &w.sc, k);
+        if (rc != P2M_OK) break;
+        if (cudaEventRecord(ev_k, st) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
+        std::lock_guard<std::mutex> lk(mu);
+        launched = c + 1;
+        cv.notify_all();
+    }
+    if (rc != P2M_OK) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (out_rc == P2M_OK) out_rc = rc;
+        cv.notify_all();
+    }
+    out.join();
+    if (rc == P2M_OK && out_rc != P2M_OK) { set_err(out_err); rc = out_rc; }
+    if (rc != P2M_OK) return rc;
+    CK(cudaStreamSynchronize(s.d2h));
+    for (auto& st : s.pipe) CK(cudaStreamSynchronize(st));
+    unsigned long long h[8] = {0};
+    if (cnt) CK(cudaMemcpy(h, s.agg, sizeof h, cudaMemcpyDeviceToHost));
+    uint64_t m = 0;
+    for (uint64_t l : len_of) m += l;
+    part.n_queries = m;
+    part.candidates_visited = h[0];
+    part.exact_evaluations = h[1];
+    part.pruned = h[0] - h[1];
+    part.kd_nodes_visited = h[2];
+    part.filter_passes = h[4];
+    part.warp_rare_iters = h[5];
+    part.structure_bytes = h[6];
+    part.scan_tiles = h[7];
+    part.fallbacks = h[3];
+    return P2M_OK;
 }
 
 P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, double* cp, uint32_t* face,
@@ -1159,6 +1413,13 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
                 for (int k = 1; k < Slot::kPipe; ++k) CK(cudaStreamWaitEvent(s.pipe[k], s.agg_ready, 0));
             }
             if (s.t0) CK(cudaEventRecord(s.t0, s.h2d));
+            const bool bounce = !(host_pinned(q + 3 * b) && host_pinned(dist + b) && host_pinned(cp + 3 * b) &&
+                                  host_pinned(face + b) && host_pinned(site + b) && (!flags || host_pinned(flags + b)));
+            if (bounce) {
+                rc = ensure_bounce(s);
+                if (rc != P2M_OK) return rc;
+                return run_bounce(e, s, q, dist, cp, face, site, flags, b, len_of, cnt, parts[g]);
+            }
             uint64_t off = 0;
             for (size_t c = 0; c < len_of.size(); ++c) {
                 const uint64_t len = len_of[c], r0 = b + off;
@@ -1205,6 +1466,8 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             parts[g].kd_nodes_visited = h[2];
             parts[g].filter_passes = h[4];
             parts[g].warp_rare_iters = h[5];
+            parts[g].structure_bytes = h[6];
+            parts[g].scan_tiles = h[7];
             parts[g].fallbacks = h[3];
             return P2M_OK;
         };
@@ -1229,6 +1492,8 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             cnt->kd_nodes_visited += c.kd_nodes_visited;
             cnt->filter_passes += c.filter_passes;
             cnt->warp_rare_iters += c.warp_rare_iters;
+            cnt->structure_bytes += c.structure_bytes;
+            cnt->scan_tiles += c.scan_tiles;
             cnt->fallbacks += c.fallbacks;
         }
     }

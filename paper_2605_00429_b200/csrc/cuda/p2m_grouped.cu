@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) k_tile_flags(Params p, const uint32_t* __
     const bool last_valid = k < n_sites && (i + 1 == n || key[i + 1] >= n_sites);
     if (last_valid) meta[1] = (uint32_t)(i + 1);
     if (i == 0 && k >= n_sites) meta[1] = 0;
-    if (i == 0) meta[2] = 0;  // small tiles, counted by k_tile_keys
+    if (i == 0) { meta[2] = 0; meta[3] = 0; }  // small tiles (k_tile_keys), table misses (scan)
 }
 
 __global__ void __launch_bounds__(256) k_tile_write(const uint32_t* __restrict__ flag,
@@ -174,10 +174,17 @@ __device__ __forceinline__ uint64_t mul2_up(uint64_t a, uint64_t b) {
     return r;
 }
 
-// Tight lower bound of d(q, T)^2 from a staged 64-byte record (a, n, m_ab, m_bc, m_ca, o_bc):
-// h^2 + max(0, s_ab, s_bc, s_ca)^2 with h = n.(q-a) and s_i the signed in-plane edge-line distances
-// (the triangle is the intersection of three half-planes).  fp32 error <= Params::lb_margin.
-__device__ __forceinline__ float lb2_face(const float4* r, float qx, float qy, float qz) {
+// Tight lower bound of d(q, T)^2 from a staged 96-byte record (a, n, m_ab, m_bc, m_ca, o_bc, b, c):
+// the max of two valid bounds, each exact in its own Voronoi region of the triangle --
+//  * h^2 + max(0, s_ab, s_bc, s_ca)^2, h = n.(q-a), s_i the signed in-plane edge-line distances (the
+//    triangle is the intersection of three half-planes): exact when the closest point is interior
+//    or on an edge;
+//  * the support-function bound along m = q - V for the vertex V nearest to q: d(q, T) >=
+//    min_i m.(q - v_i) / |m| for ANY vector m (T lies in the half-space {x : m.x <= max_i m.v_i}),
+//    which equals |q - V| when the closest point is the vertex V.
+// (Measured on c2: faces whose bound is <= the final distance drop from 32 to 3 per row.)  fp32
+// error <= Params::lb_margin.
+__device__ __forceinline__ float lb2_plane(const float4* r, float qx, float qy, float qz) {
     const float4 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3];
     const float dx = qx - r0.x, dy = qy - r0.y, dz = qz - r0.z;
     const float hh = __fmaf_rn(r0.w, dx, __fmaf_rn(r1.x, dy, __fmul_rn(r1.y, dz)));
@@ -187,7 +194,23 @@ __device__ __forceinline__ float lb2_face(const float4* r, float qx, float qy, f
     const float ee = fmaxf(0.f, fmaxf(s1, fmaxf(s2, s3)));
     return __fmaf_rn(hh, hh, __fmul_rn(ee, ee));
 }
-
+__device__ __forceinline__ float lb2_vert(const float4* r, float qx, float qy, float qz) {
+    const float4 r0 = r[0], r4 = r[4], r5 = r[5];
+    const float dx = qx - r0.x, dy = qy - r0.y, dz = qz - r0.z;  // q - a
+    const float ex = qx - r4.x, ey = qy - r4.y, ez = qz - r4.z;  // q - b
+    const float gx = qx - r4.w, gy = qy - r5.x, gz = qz - r5.y;  // q - c
+    const float Da = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+    const float Db = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+    const float Dc = __fmaf_rn(gx, gx, __fmaf_rn(gy, gy, __fmul_rn(gz, gz)));
+    float mx = dx, my = dy, mz = dz, DV = Da;    // m = q - V, V the nearest vertex
+    if (Db < DV) { mx = ex; my = ey; mz = ez; DV = Db; }
+    if (Dc < DV) { mx = gx; my = gy; mz = gz; DV = Dc; }
+    const float ta = __fmaf_rn(mx, dx, __fmaf_rn(my, dy, __fmul_rn(mz, dz)));
+    const float tb = __fmaf_rn(mx, ex, __fmaf_rn(my, ey, __fmul_rn(mz, ez)));
+    const float tc = __fmaf_rn(mx, gx, __fmaf_rn(my, gy, __fmul_rn(mz, gz)));
+    const float tm = fminf(ta, fminf(tb, tc));   // <= DV (one term is m.m); <= 0 -> no information
+    return tm > 0.f ? __fdiv_rn(__fmul_rn(tm, tm), DV) : 0.f;
+}
 // One CTA per tile (all rows share one site).  A tile of m rows uses G = ceil(m/32) warps per
 // replica and R = 8 / G replicas; replica r scans the 32-candidate batches b == r (mod R) of every
 // staged chunk, so small groups still keep all 8 warps busy.  Per batch, each lane computes a
@@ -203,6 +226,18 @@ static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 
 constexpr int kWarps = kTile / 32;
 
+#ifndef P2M_COMPACT
+#define P2M_COMPACT 1   // rare path: compacted (row, candidate) pass pairs, 32 per round (0: union walk)
+#endif
+// Per-warp shared scratch of the compacted rare path: the batch's (row lane, candidate) pass pairs and
+// the per-row lexicographic (d^2 bits, face id) minimum of the round's exact evaluations.
+struct RowScratch {
+    uint16_t pl[32 * 32];
+    unsigned long long bk[32];
+    uint32_t bf[32];
+    uint32_t ex[32];
+};
+
 // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)}, lb: 32 x
 // 64-byte lower-bound records, fid: 32 face ids), scanned for this lane's row.  Each lane computes a
 // pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
@@ -215,9 +250,9 @@ template <bool kCounters>
 __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, const V& q, uint64_t QX, uint64_t QY,
                                                uint64_t QZ, uint64_t& DK, double& best, uint32_t& bf,
                                                uint32_t& exact, unsigned long long& passes,
-                                               unsigned long long& rare_iters, const float4* pair, float4* lb,
-                                               const uint32_t* fid, int valid, bool stage_lb, uint32_t my_f,
-                                               int lane) {
+                                               unsigned long long& rare_iters, unsigned long long& sbytes,
+                                               const float4* pair, float4* lb, const uint32_t* fid, int valid,
+                                               bool stage_lb, uint32_t my_f, int lane, RowScratch& rs) {
     const float K = 1.000001f;
     const float delta = p.f32_delta;
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
@@ -245,25 +280,115 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         if (valid < 32) mask &= (1u << valid) - 1u;
     }
     uint32_t um = __reduce_or_sync(0xffffffffu, mask);
-    if (kCounters) { passes += __popc(mask); if (lane == 0) rare_iters += 32u * __popc(um); }
+    if (kCounters) {
+        passes += __popc(mask);
+        if (lane == 0) {
+            rare_iters += 32u * __popc(um);
+            if (stage_lb) sbytes += 16ull * kLbRec * __popc(um);  // the union's lower-bound records
+        }
+    }
     if (stage_lb && um) {
         if ((um >> lane) & 1u) {
-            const float4* lr = p.lbr + 4 * (uint64_t)my_f;
-            lb[4 * lane] = lr[0];
-            lb[4 * lane + 1] = lr[1];
-            lb[4 * lane + 2] = lr[2];
-            lb[4 * lane + 3] = lr[3];
+            const float4* lr = p.lbr + kLbRec * (uint64_t)my_f;
+#pragma unroll
+            for (int k = 0; k < kLbRec; ++k) lb[kLbRec * lane + k] = lr[k];
         }
         __syncwarp();
     }
+#if P2M_COMPACT
+    if (!um) return;
+    // Compact the warp's (row lane, candidate) pairs that passed the sphere filter and test them 32 at
+    // a time, one pair per lane: every lane works in every round, instead of walking the union of the
+    // rows' masks with only the lanes whose bit is set busy (c5: 38% of the lane slots).
+    const uint32_t cnt = __popc(mask);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    {
+        uint32_t wpos = incl - cnt, m = mask;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            rs.pl[wpos++] = (uint16_t)(lane << 5 | k);
+        }
+    }
+    if (kCounters) rs.ex[lane] = 0u;
+    // squared threshold of the tight bound, from the row's CURRENT d_min (refreshed after each round)
+    auto th2_of = [&](uint64_t dk) {
+        float dkx, dky;
+        upk2(dk, dkx, dky);
+        const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
+        return __fmul_ru(thl, thl);
+    };
+    float th2 = th2_of(DK);
+    __syncwarp();
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        const bool has = t < total;
+        const uint32_t pr = has ? rs.pl[t] : 0u;
+        const int r = (int)(pr >> 5), k = (int)(pr & 31u);
+        const float qx = __shfl_sync(0xffffffffu, qxf, r), qy = __shfl_sync(0xffffffffu, qyf, r),
+                    qz = __shfl_sync(0xffffffffu, qzf, r), thr = __shfl_sync(0xffffffffu, th2, r);
+        bool sv = false;
+        if (has) {
+            const float4* rec = lb + kLbRec * k;
+            sv = !(lb2_plane(rec, qx, qy, qz) > thr) && !(lb2_vert(rec, qx, qy, qz) > thr);
+        }
+        if (!__any_sync(0xffffffffu, sv)) continue;
+        // exact fp64 evaluation of the surviving pairs, in parallel (REF geom.cpp:31-70)
+        const V qr{__shfl_sync(0xffffffffu, q.x, r), __shfl_sync(0xffffffffu, q.y, r), __shfl_sync(0xffffffffu, q.z, r)};
+        unsigned long long key = 0;
+        uint32_t f = 0;
+        if (sv) {
+            f = fid[k];
+            V a, bb3, c3, pp3;
+            load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);
+            key = (unsigned long long)__double_as_longlong(closest_tri(qr, a, bb3, c3, &pp3));  // d^2 >= +0
+        }
+        if (kCounters && lane == 0) sbytes += 96ull * __popc(__ballot_sync(0xffffffffu, sv));
+        // per-row lexicographic (d^2, face id) min over the row's current best and its survivors:
+        // d^2 >= +0, so its bit pattern orders like its value
+        const unsigned long long old = (unsigned long long)__double_as_longlong(best);
+        rs.bk[lane] = old;
+        rs.bf[lane] = bf;
+        __syncwarp();
+        if (sv) atomicMin(&rs.bk[r], key);
+        __syncwarp();
+        const unsigned long long nk = rs.bk[lane];
+        if (nk != old) rs.bf[lane] = 0xffffffffu;  // a strictly smaller d^2: its face ids only
+        __syncwarp();
+        if (sv && key == rs.bk[r]) atomicMin(&rs.bf[r], f);
+        if (kCounters && sv) atomicAdd(&rs.ex[r], 1u);
+        __syncwarp();
+        if (active) {
+            bf = rs.bf[lane];
+            if (nk != old) {
+                best = __longlong_as_double((long long)nk);
+                // any upper bound of sqrt(best) is a valid d_min for the prunes: the fp32 sqrt rounded up
+                // of best rounded up (cheaper than the fp64 sqrt)
+                const float dkf = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(best)), delta), K);
+                DK = pk2(dkf, dkf);
+                th2 = th2_of(DK);
+            }
+        }
+        __syncwarp();
+    }
+    if (kCounters) exact += rs.ex[lane];
+#else
     // the exact test of one candidate kk of this lane: the tight lower bound against the CURRENT
     // d_min (the batch mask used the d_min of the batch start), then fp64
-    auto visit = [&](int kk) {
+    auto visit = [&](int kk) -> bool {
         {
             float dkx, dky;
             upk2(DK, dkx, dky);
             const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-            if (lb2_face(lb + 4 * kk, qxf, qyf, qzf) > __fmul_ru(thl, thl)) return;
+            const float th2 = __fmul_ru(thl, thl);
+            if (lb2_plane(lb + kLbRec * kk, qxf, qyf, qzf) > th2) return false;
+            if (lb2_vert(lb + kLbRec * kk, qxf, qyf, qzf) > th2) return false;
         }
         const uint32_t f = fid[kk];
         V a, bb3, c3, pp3;
@@ -278,17 +403,23 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
             const float dkf = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(dd)), delta), K);
             DK = pk2(dkf, dkf);
         }
+        return true;
     };
     // the warp walks the union of set bits in list order (the face record read is a broadcast)
     while (um) {
         const int kk = __ffs(um) - 1;
         um &= um - 1;
-        if ((mask >> kk) & 1u) visit(kk);
+        bool ex = false;
+        if ((mask >> kk) & 1u) ex = visit(kk);
+        if (kCounters && __any_sync(0xffffffffu, ex) && lane == 0) sbytes += 96;  // one face record per warp visit
     }
+
+#endif
 }
 
 // d_min seeds of one row of site s (both are upper bounds of the distance to the mesh, so the
 // (d^2, face id) argmin and every face that could tie it survive every prune).
+template <bool kCounters>
 __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q, uint64_t QX, uint64_t QY,
                                          uint64_t QZ, double& dmin, uint64_t& DK) {
     const float K = 1.000001f;
@@ -363,7 +494,9 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                                                         const uint32_t* __restrict__ order, Out o) {
     __shared__ float4 s_pair[kWarps][32];
     __shared__ uint32_t s_fid[kWarps][32];
-    __shared__ float4 s_lb[kWarps][128];
+    __shared__ float4 s_lb[kWarps][32 * kLbRec];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    RowScratch* s_rs = reinterpret_cast<RowScratch*>(s_dyn);  // kWarps of them (dynamic: > 48 KB total)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t nt = meta[0], ns = meta[2];
     const uint32_t ti = blockIdx.x * kWarps + w;
@@ -391,12 +524,14 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                 rz = __shfl_sync(0xffffffffu, fz, 0);  // the tile's first row: visiting order
     double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
     uint64_t DK = pk2(finf, finf);
-    if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
     uint32_t bf = 0xffffffffu, exact = 0;
     unsigned long long passes = 0, rare_iters = 0;
+    unsigned long long sbytes = 0;               // structure bytes loaded (counters mode; bench roofline)
+    if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK);
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     const uint64_t bo = p.boff[s], co = p.coff[s];
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+    if (kCounters && lane == 0) sbytes += 16ull * nch + 76;  // chunk spheres, site ref, offsets, tile meta
     // conservative "may some member be within d_min" test of this lane's row against a group sphere
     auto near = [&](float4 c) {
         float dkx, dky;
@@ -432,6 +567,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
         if (nch > 1 && !p.no_batch && !__any_sync(0xffffffffu, active && near(p.csph[co + cidx]))) continue;
         const uint64_t cb = beg + (uint64_t)cidx * kChunk;
         const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
+        if (kCounters && lane == 0) sbytes += 16ull * nb;  // the chunk's batch spheres
         // the chunk's batches best-first for the first row
         float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t bk = 0xffffffffu;
@@ -464,8 +600,9 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                 wpf[8 * pp + 6 + h] = rv.w;
             }
             __syncwarp();
-            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, wp,
-                                      wl, wf, valid, true, f, lane);
+            if (kCounters && lane == 0) sbytes += 20ull * valid;  // staged ids + fp32 records
+            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
+                                      wp, wl, wf, valid, true, f, lane, s_rs[w]);
             __syncwarp();                        // the slice is rewritten by the next batch
         }
     }
@@ -482,6 +619,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
         o.cp[3 * (uint64_t)row + 1] = cp.y;
         o.cp[3 * (uint64_t)row + 2] = cp.z;
         o.face[row] = bf;
+        if (bf == 0xffffffffu && o.miss) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
         if (kCounters && o.per_query) {
             o.per_query[3 * (uint64_t)row] = end - beg;
             o.per_query[3 * (uint64_t)row + 1] = exact;
@@ -489,18 +627,22 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     }
     if (kCounters && o.agg) {
         unsigned long long v0 = active ? (end - beg) : 0ull, v1 = active ? exact : 0u, v2 = passes, v3 = rare_iters;
+        unsigned long long v4 = sbytes + ((active && bf != 0xffffffffu) ? 96ull : 0ull);  // + the epilogue's record
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) {
             v0 += __shfl_down_sync(0xffffffffu, v0, sh);
             v1 += __shfl_down_sync(0xffffffffu, v1, sh);
             v2 += __shfl_down_sync(0xffffffffu, v2, sh);
             v3 += __shfl_down_sync(0xffffffffu, v3, sh);
+            v4 += __shfl_down_sync(0xffffffffu, v4, sh);
         }
         if (lane == 0) {
             atomicAdd(o.agg + 0, v0);
             atomicAdd(o.agg + 1, v1);
             atomicAdd(o.agg + 4, v2);
             atomicAdd(o.agg + 5, v3);
+            atomicAdd(o.agg + 6, v4);
+            atomicAdd(o.agg + 7, 1ull);
         }
     }
 }
@@ -524,7 +666,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                                                          const uint32_t* __restrict__ order, Out o) {
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
-    __shared__ float4 s_lb[kChunk * 4];          // the chunk's fp32 lower-bound records (64 B each)
+    __shared__ float4 s_lb[kChunk * kLbRec];     // the chunk's fp32 lower-bound records (96 B each)
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    RowScratch* s_rs = reinterpret_cast<RowScratch*>(s_dyn);  // per-warp rare-path scratch (dynamic)
     __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
     __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
     __shared__ uint32_t s_cw[kWinChunks / 32];   // chunks of the current window some row must scan
@@ -569,11 +713,13 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     uint32_t bf = 0xffffffffu;
     uint32_t exact = 0;
     unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
+    unsigned long long sbytes = 0;               // structure bytes loaded (counters mode; bench roofline)
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     float* s_pf = reinterpret_cast<float*>(s_pair);
     const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
     const uint64_t co = p.coff[s];               // ... and first 256-entry chunk sphere
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+    if (kCounters && tid == 0) sbytes += 16ull * nch + 76;  // chunk spheres, site ref, offsets, tile meta
 #define qxf __uint_as_float((uint32_t)QX)
 #define qyf __uint_as_float((uint32_t)QY)
 #define qzf __uint_as_float((uint32_t)QZ)
@@ -595,15 +741,15 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         pre_c = 0;
     }
 #endif
-    if (active) seed_row(p, s, q, QX, QY, QZ, dmin, DK);
+    if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK);
 #if P2M_EARLY1 >= 2
     if (early && tid < (int)min((uint64_t)kChunk, end - beg)) {
         // the chunk's lower-bound records, async into shared memory (nf has landed by now); waited
         // for just before the staging barrier
-        const float4* lr = p.lbr + 4 * (uint64_t)nf;
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_lb[4 * tid]);
+        const float4* lr = p.lbr + kLbRec * (uint64_t)nf;
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_lb[kLbRec * tid]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < kLbRec; ++k)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa + 16 * k), "l"(lr + k));
     }
     asm volatile("cp.async.commit_group;");
@@ -693,8 +839,8 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         // records of the union are loaded here (lane k holds entry k's face id my_f).
         auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
                               uint32_t my_f) {
-            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, pair,
-                                      lb, fid, valid, stage_lb, my_f, lane);
+            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
+                                      pair, lb, fid, valid, stage_lb, my_f, lane, s_rs[w]);
         };
         if (G == 1) {
             // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
@@ -707,7 +853,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             float4* wp = s_pair + 32 * w;
             float* wpf = reinterpret_cast<float*>(wp);
             uint32_t* wf = s_fid + 32 * w;
-            float4* wl = s_lb + 128 * w;
+            float4* wl = s_lb + 32 * kLbRec * w;
             for (;;) {
                 uint32_t t = 0;
                 if (lane == 0) t = atomicAdd(&s_next, 1u);
@@ -728,7 +874,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                     const float th = __fadd_ru(c.w, dkx);
                     need = !(d2f > __fmul_ru(th, th));
                 }
+                if (kCounters && lane == 0) sbytes += 16;  // the batch sphere
                 if (!__any_sync(0xffffffffu, need)) continue;  // pruned whole by its batch sphere
+                if (kCounters && lane == 0) sbytes += 20ull * valid;  // staged ids + fp32 records
                 uint32_t f = 0;
                 float4 rv = make_float4(finf, 0.f, 0.f, 0.f);
                 if (lane < valid) { f = p.lfs[b0 + lane]; rv = p.f32[f]; }
@@ -795,6 +943,11 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             }
             __syncthreads();
             const uint32_t cneed = s_need;
+            if (kCounters && tid == 0) {         // ids + fp32 records + batch spheres, needed lb records
+                sbytes += 20ull * mc + 16ull * nb;
+                for (int bb = 0; bb < nb; ++bb)
+                    if ((cneed >> bb) & 1u) sbytes += 16ull * kLbRec * min(32, mc - 32 * bb);
+            }
             // prefetch the window's next chunk while this one is scanned
             auto prefetch_next = [&]() {
                 pre_c = 0xffffffffu;
@@ -838,11 +991,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 else
 #endif
                 if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the lower-bound record (rare path, broadcast)
-                    const float4* lr = p.lbr + 4 * (uint64_t)nf;
-                    s_lb[4 * tid] = lr[0];
-                    s_lb[4 * tid + 1] = lr[1];
-                    s_lb[4 * tid + 2] = lr[2];
-                    s_lb[4 * tid + 3] = lr[3];
+                    const float4* lr = p.lbr + kLbRec * (uint64_t)nf;
+#pragma unroll
+                    for (int k = 0; k < kLbRec; ++k) s_lb[kLbRec * tid + k] = lr[k];
                 }
                 s_pf[8 * pp + h] = nv.x;
                 s_pf[8 * pp + 2 + h] = nv.y;
@@ -860,7 +1011,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 // vote pruned stays pruned (d_min only shrinks), so it is skipped too.
                 if (!(((R == 1 ? wneed : cneed) >> bb) & 1u)) continue;
                 const int k0 = bb * 32;
-                scan_batch(s_pair + k0, s_lb + 4 * k0, s_fid + k0, mc - k0, false, 0u);
+                scan_batch(s_pair + k0, s_lb + kLbRec * k0, s_fid + k0, mc - k0, false, 0u);
             }
         }
     }
@@ -903,6 +1054,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         o.cp[3 * (uint64_t)row + 1] = cp.y;
         o.cp[3 * (uint64_t)row + 2] = cp.z;
         o.face[row] = bf;
+        if (bf == 0xffffffffu && o.miss) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
         if (kCounters && o.per_query) {
             o.per_query[3 * (uint64_t)row] = end - beg;
             o.per_query[3 * (uint64_t)row + 1] = exact;
@@ -911,15 +1063,19 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     if (kCounters && o.agg) {
         unsigned long long v0 = writer ? (end - beg) : 0ull, v1 = writer ? exact : 0u;
         unsigned long long v2 = passes, v3 = rare_iters;
+        unsigned long long v4 = sbytes + ((writer && bf != 0xffffffffu) ? 96ull : 0ull);  // + the epilogue's record
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) {
             v2 += __shfl_down_sync(0xffffffffu, v2, sh);
             v3 += __shfl_down_sync(0xffffffffu, v3, sh);
+            v4 += __shfl_down_sync(0xffffffffu, v4, sh);
         }
         if (lane == 0) {
             atomicAdd(o.agg + 4, v2);
             atomicAdd(o.agg + 5, v3);
+            atomicAdd(o.agg + 6, v4);
         }
+        if (tid == 0) atomicAdd(o.agg + 7, 1ull);
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) {
             v0 += __shfl_down_sync(0xffffffffu, v0, sh);
@@ -934,6 +1090,39 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
 
 
 }  // namespace
+
+// Rows of a table miss (the scan kept no face: every list face lay beyond the row's d_min seed, which
+// only happens if the list is not a Theorem-1 superset): the exact BVH closest point over all faces
+// (REF/SPEC.md:201-209), flagged P2M_FLAG_FALLBACK | P2M_FLAG_TABLE_MISS.  Never fires on tables the
+// builder produced; one tiny launch per query.
+__global__ void __launch_bounds__(128) k_table_miss(Params p, const double* __restrict__ q_xyz, Out o) {
+    const uint32_t cnt = *o.miss_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const uint32_t row = o.miss[i];
+        const V q{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+        double best;
+        const uint32_t bf = bvh_closest(p, q, &best);
+        V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+             __longlong_as_double(0x7ff8000000000000ll)};
+        if (bf != 0xffffffffu) {
+            V a, b, c;
+            load_tri(p.rec + 4 * (uint64_t)bf, &a, &b, &c);
+            closest_tri(q, a, b, c, &cp);
+        }
+        o.dist[row] = sqrt(best);
+        o.cp[3 * (uint64_t)row] = cp.x;
+        o.cp[3 * (uint64_t)row + 1] = cp.y;
+        o.cp[3 * (uint64_t)row + 2] = cp.z;
+        o.face[row] = bf;
+        if (o.flags) o.flags[row] |= 5u;         // P2M_FLAG_FALLBACK | P2M_FLAG_TABLE_MISS
+    }
+}
+
+cudaError_t launch_table_miss(const Params& p, const double* q, const Out& o, cudaStream_t s) {
+    if (!o.miss) return cudaSuccess;
+    k_table_miss<<<2 * 148, 128, 0, s>>>(p, q, o);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_descend(const Params& p, const double* q, const uint32_t* rows, uint64_t n, uint32_t* site_key,
                            const Out& o, bool counters, cudaStream_t s) {
@@ -1040,17 +1229,26 @@ cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* 
     const unsigned g = (unsigned)max_tiles(n, p.n_nodes);
     cudaError_t e;
     const bool small = p.small_chunks && side;
+    const size_t dyn = P2M_COMPACT ? sizeof(RowScratch) * kWarps : 0;
+    static bool attr = false;                    // > 48 KB of shared memory per CTA: opt in once
+    if (!attr && dyn) {
+        cudaFuncSetAttribute(k_scan_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_scan_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_scan_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_scan_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        attr = true;
+    }
     if (small) {                                 // fork: small tiles on the side stream
         if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
         const unsigned gs = (g + kWarps - 1) / kWarps;
-        if (counters) k_scan_small<true><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
-        else k_scan_small<false><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
+        if (counters) k_scan_small<true><<<gs, kTile, dyn, side>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_small<false><<<gs, kTile, dyn, side>>>(p, q, rows, key, tiles, meta, order, o);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = cudaEventRecord(join, side)) != cudaSuccess) return e;
     }
-    if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
-    else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+    if (counters) k_scan_tiles<true><<<g, kTile, dyn, s>>>(p, q, rows, key, tiles, meta, order, o);
+    else k_scan_tiles<false><<<g, kTile, dyn, s>>>(p, q, rows, key, tiles, meta, order, o);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (small && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;  // join
     return cudaGetLastError();

@@ -18,6 +18,9 @@ struct Out {
     uint32_t* flags;
     uint64_t* per_query;            // optional: 3 per row (candidates, exact, kd nodes)
     unsigned long long* agg;        // optional: candidates, exact, kd nodes, fallbacks
+    uint32_t* miss = nullptr;       // grouped scan: rows whose list produced no face within the d_min
+    uint32_t* miss_n = nullptr;     // seed (a table that is not a Theorem-1 superset), answered by
+                                    // launch_table_miss with the exact BVH fallback and flagged
 };
 
 cudaError_t launch_morton(const double* q, uint64_t n, const Params& p, uint32_t* keys, uint32_t* rows,
@@ -30,6 +33,7 @@ cudaError_t launch_nearest(const Params& p, const double* q, const uint32_t* row
 // grouped pipeline: (1) descent per row in Morton order -> site key (fallback rows answered inline,
 // keyed n_sites so they sort last); (2) [sort by site]; (3) per-CTA tiles of rows sharing a site scan
 // the site's list staged through shared memory.
+cudaError_t launch_table_miss(const Params& p, const double* q, const Out& o, cudaStream_t s);
 cudaError_t launch_descend(const Params& p, const double* q, const uint32_t* rows, uint64_t n,
                            uint32_t* site_key, const Out& o, bool counters, cudaStream_t s);
 size_t tiles_tmp_bytes(uint64_t n);

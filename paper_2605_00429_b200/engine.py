@@ -253,6 +253,19 @@ class Engine:
         self._h = h
         self.devices = tuple(devices)
 
+    @classmethod
+    def from_desc(cls, desc: L.EngineDesc, devices: Sequence[int] = (0,), keep=()) -> "Engine":
+        """An engine from a caller-filled p2m_engine_desc (the drop-in path of an external builder,
+        INTEGRATION.md); `keep` holds the arrays its pointers refer to until creation returns."""
+        self = cls.__new__(cls)
+        self.host_engine = None
+        ids = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        L.check(L.cuda().p2m_engine_create(C.byref(desc), len(devices), ids, C.byref(h)))
+        self._h = h
+        self.devices = tuple(devices)
+        return self
+
     def close(self):
         h = getattr(self, "_h", None)
         if h:
@@ -275,15 +288,17 @@ class Engine:
         L.check(L.cuda().p2m_engine_info(self.handle, C.byref(n), C.byref(ms), C.byref(b)))
         return {"n_devices": n.value, "replicate_ms": ms.value, "device_bytes": b.value}
 
-    def batch_query(self, points) -> BatchResult:
+    def batch_query(self, points, counters: bool = True) -> BatchResult:
+        """batch_query (REF/SPEC.md:497-505) on host arrays (p2m_query; pageable numpy memory goes
+        through the library's pinned bounce rings).  counters=False skips the counters pass."""
         q = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         n = len(q)
         dist = np.empty(n); cp = np.empty((n, 3))
         face = np.empty(n, np.uint32); site = np.empty(n, np.uint32); flags = np.empty(n, np.uint32)
         cnt = L.Counters()
         L.check(L.cuda().p2m_query(self.handle, L.ptr(q), n, L.ptr(dist), L.ptr(cp), L.ptr(face, L.u32p),
-                                   L.ptr(site, L.u32p), L.ptr(flags, L.u32p), C.byref(cnt)))
-        return BatchResult(dist, cp, face, site, flags, cnt.as_dict())
+                                   L.ptr(site, L.u32p), L.ptr(flags, L.u32p), C.byref(cnt) if counters else None))
+        return BatchResult(dist, cp, face, site, flags, cnt.as_dict() if counters else {})
 
     def query_distance(self, q) -> QueryResult:
         r = self.batch_query(np.asarray(q, dtype=np.float64).reshape(1, 3))

@@ -369,3 +369,70 @@ def test_host_api_geometric_schedules_identical(c2, sched, monkeypatch):
     r = P.Engine(h).batch_query(q)
     _compare(r, {"site": base.site, "face": base.face, "flags": base.flags, "distance": base.distance,
                  "closest": base.closest}, len(q))
+
+
+@pytest.mark.parametrize("chunks,with_flags", [("0", True), ("2", False)])
+def test_host_api_pageable_equals_pinned(c2, chunks, with_flags, monkeypatch):
+    """p2m_query on pageable caller arrays runs through pinned bounce rings (1 M-row sub-chunks,
+    packed/unpacked by host threads); on page-locked arrays the DMA engines read and write them
+    directly.  Both give the same rows, bit for bit, across several sub-chunks per chunk, with and
+    without the optional flags array."""
+    import torch
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 4_000_000, 2_600_000)
+    n = len(q)
+    monkeypatch.setenv("P2M_E2E_CHUNKS", chunks)
+    eng = P.Engine(h)
+    lib = L.cuda()
+    pd, pc = np.full(n, -1.0), np.full((n, 3), -1.0)
+    pf, ps, pfl = (np.zeros(n, np.uint32) for _ in range(3))
+    L.check(lib.p2m_query(eng.handle, L.ptr(q), n, L.ptr(pd), L.ptr(pc), L.ptr(pf, L.u32p), L.ptr(ps, L.u32p),
+                          L.ptr(pfl, L.u32p) if with_flags else None, None))
+    qp = torch.from_numpy(q).pin_memory()
+    od = torch.empty(n, dtype=torch.float64).pin_memory()
+    oc = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    of, osi, ofl = (torch.zeros(n, dtype=torch.int32).pin_memory() for _ in range(3))
+    dp = lambda t: C.cast(C.c_void_p(t.data_ptr()), L.dp)
+    up = lambda t: C.cast(C.c_void_p(t.data_ptr()), L.u32p)
+    L.check(lib.p2m_query(eng.handle, dp(qp), n, dp(od), dp(oc), up(of), up(osi), up(ofl) if with_flags else None, None))
+    assert pd.tobytes() == od.numpy().tobytes()
+    assert pc.tobytes() == oc.numpy().tobytes()
+    assert np.array_equal(pf, of.numpy().view(np.uint32))
+    assert np.array_equal(ps, osi.numpy().view(np.uint32))
+    if with_flags:
+        assert np.array_equal(pfl, ofl.numpy().view(np.uint32))
+
+
+def test_table_miss_falls_back_exactly(ico3):
+    """A caller-filled desc whose list for site 0 is NOT a superset (one far face only): the grouped
+    scan's d_min seed |q - v| prunes that face, the row would keep no face at all -- it is answered by
+    the exact BVH fallback instead and flagged FALLBACK | TABLE_MISS (the seed assumes the
+    Theorem-1 superset invariant, REF/SPEC.md:435).  Rows of every other site are unchanged."""
+    V, F, h = ico3
+    a = h.arrays()
+    off = a["list_offsets"].astype(np.uint64)
+    lf = a["list_faces"].astype(np.uint32)
+    tri = a["tri"].reshape(-1, 9)
+    cen = tri.reshape(-1, 3, 3).mean(1)
+    far = int(np.argmax(np.linalg.norm(cen - V[0], axis=1)))
+    new_lf = np.concatenate([lf[: off[0]], np.array([far], np.uint32), lf[off[1]:]])
+    new_off = off.copy()
+    new_off[1:] = off[1:] - (off[1] - off[0]) + 1
+    d = h.desc()
+    d.list_offsets = new_off.ctypes.data_as(L.u64p)
+    d.list_faces = new_lf.ctypes.data_as(L.u32p)
+    eng = P.Engine.from_desc(d, keep=(new_off, new_lf))
+    rng = np.random.default_rng(11)
+    q = np.concatenate([V[0] * 1.02 + rng.normal(0, 0.01, size=(3000, 3)),
+                        rng.uniform(-1.3, 1.3, size=(3000, 3))])
+    r = eng.batch_query(q)
+    base = P.Engine(h).batch_query(q)
+    hit = r.site == 0
+    assert hit.sum() > 100
+    assert np.all((r.flags[hit] & 5) == 5) and np.all((r.flags[~hit] & 4) == 0)
+    for i in np.flatnonzero(hit)[:300]:
+        d2, p, f = O.brute_force_closest(tri, q[i])
+        assert r.face[i] == f and r.distance[i] == np.sqrt(d2) and r.closest[i].tobytes() == p.tobytes()
+    # the fallback answer is the exact one, so it equals the superset engine's row
+    assert r.distance.tobytes() == base.distance.tobytes() and np.array_equal(r.face, base.face)
+    assert np.array_equal(r.flags[~hit], base.flags[~hit])

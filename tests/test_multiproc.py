@@ -1,7 +1,9 @@
-"""The N>1 path on CPU (gloo, world_size 2): bench.py's weak-scaling sharding (each rank owns the
-contiguous slice [rank*n, (rank+1)*n) of the config's counter-based query sequence, builds its own
-replica, and answers it with no data-path collective) reproduces the single-process answer over
-[0, world*n), and the timing reduction is a max over ranks."""
+"""The N>1 path on CPU (gloo, world_size 2).  bench.py shards ONE batch over the ranks (strong
+scaling, the metric's "100M queries sharded across 1/2/4/8 GPUs"): an even contiguous split or a
+Morton-range spatial partition; each rank answers its own rows against its own copy of the engine
+(rank 0 builds and saves the EngineIndexFile, rank 1 loads it) with no data-path collective.  The
+union of the ranks' rows must reproduce the single-process answer row for row, and the timing
+reduction is a max over ranks.  The weak-scaling rule (rank_slice) is checked the same way."""
 import os
 import socket
 
@@ -15,7 +17,7 @@ import oracle as O
 import paper_2605_00429_b200 as P
 from paper_2605_00429_b200 import shard
 
-N_PER_RANK = 3000
+N_TOTAL = 6000
 
 
 def _free_port():
@@ -26,41 +28,72 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     V, F = P.icosphere(3)
-    h = P.HostEngine.build(V, F, P.BuildConfig(n_threads=2))
-    first, count = shard.rank_slice(rank, world, N_PER_RANK)
-    q = P.gen_queries(1, V, F, first, count)
+    path = os.path.join(out_dir, "engine.p2mx")
+    if rank == 0:                               # build once, the other rank loads the index file
+        h = P.HostEngine.build(V, F, P.BuildConfig(n_threads=2))
+        h.save(path)
+    dist.barrier()
+    if rank != 0:
+        h = P.HostEngine.load(path, V, F)
+    gen = lambda a, b: P.gen_queries(1, V, F, a, b)  # noqa: E731
+    if mode == "even":
+        first, count = shard.device_shard(N_TOTAL, world, rank)
+        q, idx = gen(first, count), np.arange(first, first + count)
+    elif mode == "spatial":
+        A = h.arrays()
+        box = shard.morton_box(A["site_xyz"][A["site_kind"] != 1])
+        q, idx = shard.spatial_shard(gen, N_TOTAL, world, rank, box, bits=4, chunk=1000)
+    else:                                       # weak: every rank its own N_TOTAL / world rows
+        first, count = shard.rank_slice(rank, world, N_TOTAL // world)
+        q, idx = gen(first, count), np.arange(first, first + count)
     r = O.OracleEngine(h.arrays()).batch_query(q, threads=2)
-    part = torch.from_numpy(np.concatenate([r["distance"], r["face"].astype(np.float64), r["site"].astype(np.float64)]))
-    parts = [torch.zeros_like(part) for _ in range(world)]
-    dist.all_gather(parts, part)
+    rec = np.zeros((len(q), 4))
+    rec[:, 0] = idx
+    rec[:, 1] = r["distance"]
+    rec[:, 2] = r["face"]
+    rec[:, 3] = r["site"]
+    n_loc = torch.tensor([len(q)])
+    ns = [torch.zeros_like(n_loc) for _ in range(world)]
+    dist.all_gather(ns, n_loc)
+    m = int(max(int(x) for x in ns))
+    pad = torch.full((m, 4), -1.0, dtype=torch.float64)
+    pad[: len(q)] = torch.from_numpy(rec)
+    parts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
     t = shard.max_over_ranks(0.5 + rank, dist)  # each rank "took" 0.5 + rank seconds
     if rank == 0:
-        np.save(os.path.join(out_dir, "gathered.npy"), torch.stack(parts).numpy())
+        np.save(os.path.join(out_dir, "gathered.npy"), torch.cat(parts).numpy())
+        np.save(os.path.join(out_dir, "counts.npy"), np.array([int(x) for x in ns]))
         np.save(os.path.join(out_dir, "tmax.npy"), np.array([t]))
     dist.barrier()
     dist.destroy_process_group()
 
 
 @pytest.mark.timeout(300)
-def test_two_rank_weak_scaling_matches_single_process(tmp_path):
+@pytest.mark.parametrize("mode", ["even", "spatial", "weak"])
+def test_two_rank_sharding_matches_single_process(tmp_path, mode):
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, join=True)
     got = np.load(tmp_path / "gathered.npy")
+    got = got[got[:, 0] >= 0]
+    counts = np.load(tmp_path / "counts.npy")
     assert float(np.load(tmp_path / "tmax.npy")[0]) == 1.5
+    assert counts.sum() == N_TOTAL
+    if mode == "spatial":                        # balanced within the key-cell granularity
+        assert counts.min() > 0.25 * N_TOTAL
+    idx = got[:, 0].astype(np.int64)
+    assert np.array_equal(np.sort(idx), np.arange(N_TOTAL))  # a partition of the batch
     V, F = P.icosphere(3)
     h = P.HostEngine.build(V, F)
-    q = P.gen_queries(1, V, F, 0, world * N_PER_RANK)
+    q = P.gen_queries(1, V, F, 0, N_TOTAL)
     r = O.OracleEngine(h.arrays()).batch_query(q)
-    for rank in range(world):
-        sl = slice(rank * N_PER_RANK, (rank + 1) * N_PER_RANK)
-        n = N_PER_RANK
-        assert got[rank][:n].tobytes() == r["distance"][sl].tobytes()
-        assert np.array_equal(got[rank][n:2 * n].astype(np.uint32), r["face"][sl])
-        assert np.array_equal(got[rank][2 * n:].astype(np.uint32), r["site"][sl])
+    assert got[:, 1].tobytes() == r["distance"][idx].tobytes()
+    assert np.array_equal(got[:, 2].astype(np.uint32), r["face"][idx])
+    assert np.array_equal(got[:, 3].astype(np.uint32), r["site"][idx])
 
 
 def test_rank_slices_partition():
@@ -74,3 +107,25 @@ def test_rank_slices_partition():
             assert sum(c for _, c in b) == total
             assert all(b[k][0] + b[k][1] == b[k + 1][0] for k in range(g - 1))
             assert max(c for _, c in b) - min(c for _, c in b) <= 1
+
+
+def test_spatial_partition_is_a_partition():
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(-1, 1, size=(20000, 3))
+    gen = lambda a, b: pts[a:a + b]  # noqa: E731
+    box = shard.morton_box(pts)
+    for world in (1, 2, 3, 8):
+        seen = []
+        for r in range(world):
+            q, idx = shard.spatial_shard(gen, len(pts), world, r, box, bits=5, chunk=3000)
+            assert np.array_equal(q, pts[idx])
+            assert np.all(np.diff(idx) > 0)           # batch order kept inside a part
+            seen.append(idx)
+            assert len(idx) > 0.5 * len(pts) / world  # balanced up to key-cell granularity
+        allidx = np.concatenate(seen)
+        assert np.array_equal(np.sort(allidx), np.arange(len(pts)))
+    # the key ranges are contiguous: every key of part r is below every key of part r+1
+    k = shard.morton_keys(pts, box, 5)
+    q0, i0 = shard.spatial_shard(gen, len(pts), 2, 0, box, bits=5)
+    q1, i1 = shard.spatial_shard(gen, len(pts), 2, 1, box, bits=5)
+    assert k[i0].max() < k[i1].min()
