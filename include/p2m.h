@@ -115,6 +115,17 @@ int p2m_engine_create(const p2m_engine_desc *desc, int n_devices, const int *dev
                       p2m_engine **out);
 void p2m_engine_destroy(p2m_engine *engine);
 
+/* Device image of an engine (the EngineIndexFile loaded straight into the
+ * device layout; REF/SPEC.md:588-591, 637-641).  save writes slot 0's packed layout -- k-d tree,
+ * face records, fp32 records, spatially ordered lists with their group spheres, cell-locate grid,
+ * fallback BVH, heavy-site flags, kernel parameters -- as "P2MD" v1 (little-endian, FNV-1a
+ * checksum).  load validates every count, CSR and id range, then uploads it as is (no host desc,
+ * no re-packing, no heavy-site estimate) and replicates it like p2m_engine_create.  Queries on a
+ * loaded engine are bit-identical to the engine that was saved.  Errors: P2M_ERR_IO (open, magic,
+ * version, truncation, checksum, invalid contents), P2M_ERR_CUDA. */
+int p2m_engine_save(const p2m_engine *engine, const char *path);
+int p2m_engine_load(const char *path, int n_devices, const int *device_ids, p2m_engine **out);
+
 /* Number of devices the engine is replicated on, and the peer-replica timing of create. */
 int p2m_engine_info(const p2m_engine *engine, int *n_devices, double *replicate_ms,
                     uint64_t *device_bytes);

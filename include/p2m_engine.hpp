@@ -97,6 +97,14 @@ class Engine {
         p2m_engine_desc d = host.desc();
         check(p2m_engine_create(&d, (int)devices.size(), devices.data(), &e_));
     }
+    // straight from a device image (p2m_engine_load): no host engine, no re-packing
+    static Engine load(const std::string& path, const std::vector<int>& devices = {0}) {
+        Engine e;
+        check(p2m_engine_load(path.c_str(), (int)devices.size(), devices.data(), &e.e_));
+        return e;
+    }
+    void save(const std::string& path) const { check(p2m_engine_save(e_, path.c_str())); }
+    Engine(Engine&& o) noexcept : e_(o.e_) { o.e_ = nullptr; }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
     ~Engine() { p2m_engine_destroy(e_); }
@@ -118,6 +126,7 @@ class Engine {
     p2m_engine* handle() const { return e_; }
 
    private:
+    Engine() = default;
     p2m_engine* e_ = nullptr;
 };
 

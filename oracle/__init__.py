@@ -47,6 +47,7 @@ def _bind(L):
     L.orc_nearest_site_brute.argtypes = [dp, C.c_uint64, dp, dp]
     L.orc_brute_force_closest.restype = C.c_uint32
     L.orc_brute_force_closest.argtypes = [dp, C.c_uint64, dp, dp, dp]
+    L.orc_batch_brute_force.argtypes = [dp, C.c_uint64, dp, C.c_uint64, C.c_int, dp, dp, u32p]
     L.orc_ctx_create.restype = C.c_void_p
     L.orc_ctx_create.argtypes = [C.c_uint64, dp, u8p, C.c_uint64, dp, dp, u64p, u32p, dp]
     L.orc_ctx_free.argtypes = [C.c_void_p]
@@ -124,6 +125,17 @@ def brute_force_closest(tri, q, reference=False):
     d2 = np.zeros(1); p = np.zeros(3)
     f = L.orc_brute_force_closest(_p(tri), len(tri), _p(q), _p(d2), _p(p))
     return float(d2[0]), p, int(f)
+
+
+def batch_brute_force(tri, q, reference=False, threads=0):
+    """brute_force_closest for every row of q (OpenMP): {'d2', 'closest', 'face'}."""
+    L = lib(reference)
+    tri = np.ascontiguousarray(tri, dtype=np.float64).reshape(-1, 9)
+    q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
+    n = len(q)
+    d2 = np.zeros(n); p = np.zeros((n, 3)); f = np.zeros(n, np.uint32)
+    L.orc_batch_brute_force(_p(tri), len(tri), _p(q), n, threads, _p(d2), _p(p), _p(f, u32p))
+    return {"d2": d2, "closest": p, "face": f}
 
 
 def nearest_site_brute(sites, q, reference=False):

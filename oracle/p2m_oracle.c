@@ -377,6 +377,16 @@ ORC_EXPORT uint32_t orc_brute_force_closest(const double *tri, uint64_t nf, cons
     return bf;
 }
 
+/* brute_force_closest over a batch of queries (OpenMP over queries): the table-independent arbiter
+ * of the acceptance check (REF/SPEC.md:508, 536-544, 665-667) on sampled queries. */
+ORC_EXPORT void orc_batch_brute_force(const double *tri, uint64_t nf, const double *q, uint64_t n, int threads,
+                                      double *d2_out, double *p_out, uint32_t *face_out) {
+    if (threads <= 0) threads = omp_get_max_threads();
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 16)
+    for (int64_t i = 0; i < (int64_t)n; ++i)
+        face_out[i] = orc_brute_force_closest(tri, nf, q + 3 * i, d2_out + i, p_out + 3 * i);
+}
+
 /* ------------------------------------------------------------------------------------------
  * Engine context: the engine arrays are caller-owned (the same bytes the GPU consumes); the
  * oracle derives only its own k-d tree from the site positions.

@@ -185,6 +185,8 @@ def cuda() -> C.CDLL:
         vp = C.c_void_p
         L.p2m_engine_create.argtypes = [C.POINTER(EngineDesc), C.c_int, C.POINTER(C.c_int), C.POINTER(vp)]
         L.p2m_engine_destroy.argtypes = [vp]
+        L.p2m_engine_save.argtypes = [vp, C.c_char_p]
+        L.p2m_engine_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_int), C.POINTER(vp)]
         L.p2m_engine_info.argtypes = [vp, C.POINTER(C.c_int), dp, u64p]
         L.p2m_query.argtypes = [vp, dp, C.c_uint64, dp, dp, u32p, u32p, u32p, C.POINTER(Counters)]
         L.p2m_query_device.argtypes = [vp, C.c_int, vp, C.c_uint64, vp, vp, vp, vp, vp, vp, C.POINTER(Counters)]

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <type_traits>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -680,7 +681,7 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
 // scan and count the exact point-triangle evaluations.  Sites whose estimate reaches the threshold
 // (deep auxiliary sites of closed surfaces, where the distance field is flat and sphere pruning
 // cannot cut the list) get short tiles so their rows spread over many SMs.
-int mark_heavy_sites(p2m_engine* E, const p2m_engine_desc* d) {
+int mark_heavy_sites(p2m_engine* E, const double* site_xyz, const uint8_t* site_kind) {
     uint32_t thr = 1024;
     if (const char* v = std::getenv("P2M_HEAVY_E")) thr = (uint32_t)std::strtoul(v, nullptr, 10);
     const uint64_t S = E->n_sites;
@@ -691,7 +692,7 @@ int mark_heavy_sites(p2m_engine* E, const p2m_engine_desc* d) {
     uint64_t* pq = nullptr;
     CK(cudaMalloc(&q, 24 * S)); CK(cudaMalloc(&dist, 8 * S)); CK(cudaMalloc(&cp, 24 * S));
     CK(cudaMalloc(&face, 4 * S)); CK(cudaMalloc(&site, 4 * S)); CK(cudaMalloc(&pq, 24 * S));
-    CK(cudaMemcpy(q, d->site_xyz, 24 * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(q, site_xyz, 24 * S, cudaMemcpyHostToDevice));
     const int mode = E->scan_mode;
     const bool prof = E->profiling;
     E->scan_mode = P2M_SCAN_FUSED;
@@ -710,12 +711,124 @@ int mark_heavy_sites(p2m_engine* E, const p2m_engine_desc* d) {
     std::vector<uint8_t> heavy(S, 0);
     uint64_t n_heavy = 0;
     for (uint64_t i = 0; i < S; ++i)
-        if (d->site_kind[i] != P2M_SITE_SENTINEL && h[3 * i + 1] >= thr) { heavy[i] = 1; ++n_heavy; }
+        if (site_kind[i] != P2M_SITE_SENTINEL && h[3 * i + 1] >= thr) { heavy[i] = 1; ++n_heavy; }
     E->n_heavy = n_heavy;
     for (auto& s : E->slots) {
         CK(cudaSetDevice(s->dev));
         CK(cudaMemcpy(s->heavy, heavy.data(), S, cudaMemcpyHostToDevice));
     }
+    return P2M_OK;
+}
+
+
+// The packed device layout of one replica as host arrays: what p2m_engine_create derives from a
+// p2m_engine_desc, and what a device image file (p2m_engine_save / p2m_engine_load) stores.
+struct Image {
+    template <class T>
+    struct Arr {
+        const T* p = nullptr;
+        uint64_t n = 0;
+        std::vector<T> own;
+        void set(const T* q, uint64_t m) { p = q; n = m; }
+        void take(std::vector<T>&& v) { own = std::move(v); p = own.data(); n = own.size(); }
+        uint64_t bytes() const { return sizeof(T) * n; }
+    };
+    Arr<D4> kd, rec, bvh, site_pos, site_ref;
+    Arr<float4> f32, bsph, csph, lbr;
+    Arr<uint64_t> boff, coff, off, adj_off;
+    Arr<uint32_t> lf, lfs, bvh_perm, grid_off, grid_site, adj;
+    Arr<uint8_t> heavy;   // empty: estimate at creation (mark_heavy_sites)
+};
+
+// Allocate the slots, upload the image to the first device, replicate it to the others by a one-time
+// peer copy, set the kernel parameters and the schedule knobs; E's counts must be set.
+int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices, const int* device_ids, int ndev) {
+    const uint64_t S = E->n_sites, F = E->n_faces;
+    for (int k = 0; k < n_devices; ++k) {
+        auto s = std::make_unique<Slot>();
+        s->dev = device_ids ? device_ids[k] : k;
+        if (s->dev < 0 || s->dev >= ndev) { set_err("p2m_engine_create: bad device id"); return P2M_ERR_INVALID; }
+        E->slots.push_back(std::move(s));
+    }
+    for (auto& s : E->slots) {
+        int rc = alloc_slot(*s, *E);
+        if (rc != P2M_OK) return rc;
+    }
+    Slot& s0 = *E->slots[0];
+    struct Up { void* dst; const void* src; size_t n; };
+    auto uploads = [&](Slot& s) {
+        return std::vector<Up>{
+            {s.kd, I.kd.p, I.kd.bytes()}, {s.rec, I.rec.p, I.rec.bytes()}, {s.f32, I.f32.p, I.f32.bytes()},
+            {s.bsph, I.bsph.p, I.bsph.bytes()}, {s.boff, I.boff.p, I.boff.bytes()}, {s.lbr, I.lbr.p, I.lbr.bytes()},
+            {s.off, I.off.p, I.off.bytes()}, {s.lf, I.lf.p, I.lf.bytes()}, {s.lfs, I.lfs.p, I.lfs.bytes()},
+            {s.csph, I.csph.p, I.csph.bytes()}, {s.coff, I.coff.p, I.coff.bytes()}, {s.bvh, I.bvh.p, I.bvh.bytes()},
+            {s.bvh_perm, I.bvh_perm.p, I.bvh_perm.bytes()}, {s.site_pos, I.site_pos.p, I.site_pos.bytes()},
+            {s.site_ref, I.site_ref.p, I.site_ref.bytes()},
+            {s.adj_off, I.adj_off.p, E->has_adj ? I.adj_off.bytes() : 0}, {s.adj, I.adj.p, E->has_adj ? I.adj.bytes() : 0},
+            {s.grid_off, I.grid_off.p, E->grid_cells ? I.grid_off.bytes() : 0},
+            {s.grid_site, I.grid_site.p, E->grid_cells ? I.grid_site.bytes() : 0},
+            {s.heavy, I.heavy.p, I.heavy.bytes()}};
+    };
+    {
+        CK(cudaSetDevice(s0.dev));
+        for (const Up& u : uploads(s0))
+            if (u.n && cudaMemcpy(u.dst, u.src, u.n, cudaMemcpyHostToDevice) != cudaSuccess) {
+                set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
+                return P2M_ERR_CUDA;
+            }
+    }
+    E->bytes = 0;
+    for (const Up& u : uploads(s0)) E->bytes += u.n;
+    auto t0 = std::chrono::steady_clock::now();
+    for (size_t k = 1; k < E->slots.size(); ++k) {
+        Slot& s = *E->slots[k];
+        cudaSetDevice(s.dev);
+        if (s.dev != s0.dev) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, s.dev, s0.dev);
+            if (can) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(s0.dev, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) { set_err("peer access failed"); return P2M_ERR_CUDA; }
+                cudaGetLastError();
+            }
+        }
+        const std::vector<Up> dst = uploads(s), src = uploads(s0);
+        for (size_t i = 0; i < dst.size(); ++i)
+            if (dst[i].n && cudaMemcpyPeerAsync(dst[i].dst, s.dev, src[i].dst, s0.dev, dst[i].n, s.stream) != cudaSuccess) {
+                set_err("p2m_engine_create: peer copy failed");
+                return P2M_ERR_CUDA;
+            }
+    }
+    for (auto& s : E->slots) {
+        cudaSetDevice(s->dev);
+        if (cudaStreamSynchronize(s->stream) != cudaSuccess) { set_err("p2m_engine_create: replica sync failed"); return P2M_ERR_CUDA; }
+    }
+    E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& s : E->slots) {
+        s->params = P;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.lbr = s->lbr; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.lfs = s->lfs; s->params.csph = s->csph; s->params.coff = s->coff;
+        s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
+        s->params.site_pos = s->site_pos;
+        s->params.site_ref = s->site_ref;
+        s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
+        s->params.grid_site = s->grid_site;
+        s->params.nns = P2M_NNS_GRID;
+        s->params.tile_order = -1;
+        s->params.small_chunks = 2;  // measured on c2 (1, 2 > 4) and c5 (2 ~ 4 > 0)
+        if (const char* v = std::getenv("P2M_SMALL_CHUNKS")) s->params.small_chunks = (uint32_t)std::min(4, std::max(0, std::atoi(v)));
+        if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
+        s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
+        s->params.adj = s->adj;
+    }
+    if (const char* v = std::getenv("P2M_MORTON_BITS")) E->morton_bits = std::min(30, std::max(3, std::atoi(v)));
+    if (const char* v = std::getenv("P2M_E2E_SCHED")) {
+        double x[4];
+        if (std::sscanf(v, "%lf,%lf,%lf,%lf", &x[0], &x[1], &x[2], &x[3]) == 4 && x[0] > 0 && x[1] >= 1 && x[2] > 0 &&
+            x[3] >= 0 && x[3] < 1)
+            for (int k = 0; k < 4; ++k) E->e2e_sched[k] = x[k];
+    }
+    if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(0, std::atoi(v));
     return P2M_OK;
 }
 
@@ -999,111 +1112,216 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         }
     }
     // ---- upload to the first device, peer-replicate to the rest ----
-    for (int k = 0; k < n_devices; ++k) {
-        auto s = std::make_unique<Slot>();
-        s->dev = device_ids ? device_ids[k] : k;
-        if (s->dev < 0 || s->dev >= ndev) { set_err("p2m_engine_create: bad device id"); return P2M_ERR_INVALID; }
-        E->slots.push_back(std::move(s));
-    }
-    for (auto& s : E->slots) {
-        int rc = alloc_slot(*s, *E);
-        if (rc != P2M_OK) { for (auto& x : E->slots) free_slot(*x); return rc; }
-    }
-    Slot& s0 = *E->slots[0];
+    Image I;
+    I.kd.set(kd.data(), S); I.rec.set(rec.data(), 4 * F); I.f32.set(f32.data(), F);
+    I.bsph.set(bsph.data(), bsph.size()); I.boff.set(boff.data(), S + 1); I.lbr.set(lbr.data(), lbr.size());
+    I.off.set(d->list_offsets, S + 1); I.lf.set(d->list_faces, L); I.lfs.set(lfs.data(), L);
+    I.csph.set(csph.data(), csph.size()); I.coff.set(coff.data(), S + 1);
+    I.bvh.set(bvh.nodes.data(), bvh.nodes.size()); I.bvh_perm.set(bvh.perm.data(), F);
+    I.site_pos.set(site_pos.data(), S); I.site_ref.set(site_ref.data(), S);
+    if (E->has_adj) { I.adj_off.set(d->adj_offsets, S + 1); I.adj.set(d->adj_sites, E->n_adj); }
+    if (E->grid_cells) { I.grid_off.set(grid.off.data(), E->grid_cells + 1); I.grid_site.set(grid.site.data(), E->grid_pairs); }
     auto fail = [&](int rc) { for (auto& x : E->slots) free_slot(*x); return rc; };
     {
-        cudaSetDevice(s0.dev);
-        if (cudaMemcpy(s0.kd, kd.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.rec, rec.data(), sizeof(D4) * 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.f32, f32.data(), sizeof(float4) * F, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.bsph, bsph.data(), sizeof(float4) * bsph.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.boff, boff.data(), 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.lbr, lbr.data(), sizeof(float4) * lbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.off, d->list_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
-            (L && cudaMemcpy(s0.lf, d->list_faces, 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
-            (L && cudaMemcpy(s0.lfs, lfs.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess) ||
-            cudaMemcpy(s0.csph, csph.data(), sizeof(float4) * csph.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.coff, coff.data(), 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.bvh, bvh.nodes.data(), sizeof(D4) * bvh.nodes.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.bvh_perm, bvh.perm.data(), 4 * F, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.site_pos, site_pos.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(s0.site_ref, site_ref.data(), sizeof(D4) * S, cudaMemcpyHostToDevice) != cudaSuccess ||
-            (E->has_adj && cudaMemcpy(s0.adj_off, d->adj_offsets, 8 * (S + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
-            (E->n_adj && cudaMemcpy(s0.adj, d->adj_sites, 4 * E->n_adj, cudaMemcpyHostToDevice) != cudaSuccess) ||
-            (E->grid_cells && cudaMemcpy(s0.grid_off, grid.off.data(), 4 * (E->grid_cells + 1), cudaMemcpyHostToDevice) != cudaSuccess) ||
-            (E->grid_pairs && cudaMemcpy(s0.grid_site, grid.site.data(), 4 * E->grid_pairs, cudaMemcpyHostToDevice) != cudaSuccess)) {
-            set_err(std::string("p2m_engine_create: upload failed: ") + cudaGetErrorString(cudaGetLastError()));
-            return fail(P2M_ERR_CUDA);
-        }
-    }
-    E->bytes = sizeof(D4) * (3 * S + 4 * F + bvh.nodes.size()) + sizeof(float4) * (5 * F + E->n_batches + E->n_chunks) +
-               3 * 8 * (S + 1) + 4 * (2 * L + F) + S +
-               (E->grid_cells ? 4 * (E->grid_cells + 1 + E->grid_pairs) : 0) + (E->has_adj ? 8 * (S + 1) + 4 * E->n_adj : 0);
-    auto t0 = std::chrono::steady_clock::now();
-    for (size_t k = 1; k < E->slots.size(); ++k) {
-        Slot& s = *E->slots[k];
-        cudaSetDevice(s.dev);
-        if (s.dev != s0.dev) {
-            int can = 0;
-            cudaDeviceCanAccessPeer(&can, s.dev, s0.dev);
-            if (can) {
-                cudaError_t e = cudaDeviceEnablePeerAccess(s0.dev, 0);
-                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) { set_err("peer access failed"); return fail(P2M_ERR_CUDA); }
-                cudaGetLastError();
-            }
-        }
-        struct { void* dst; const void* src; size_t n; } cp[] = {
-            {s.kd, s0.kd, sizeof(D4) * S}, {s.rec, s0.rec, sizeof(D4) * 4 * F}, {s.f32, s0.f32, sizeof(float4) * F},
-            {s.bsph, s0.bsph, sizeof(float4) * std::max<uint64_t>(1, E->n_batches)}, {s.boff, s0.boff, 8 * (S + 1)},
-            {s.lbr, s0.lbr, sizeof(float4) * kLbRec * std::max<uint64_t>(1, F)},
-            {s.off, s0.off, 8 * (S + 1)},
-            {s.lf, s0.lf, 4 * L}, {s.lfs, s0.lfs, 4 * L},
-            {s.csph, s0.csph, sizeof(float4) * std::max<uint64_t>(1, E->n_chunks)}, {s.coff, s0.coff, 8 * (S + 1)},
-            {s.bvh, s0.bvh, sizeof(D4) * bvh.nodes.size()}, {s.bvh_perm, s0.bvh_perm, 4 * F},
-            {s.site_pos, s0.site_pos, sizeof(D4) * S}, {s.site_ref, s0.site_ref, sizeof(D4) * S},
-            {s.grid_off, s0.grid_off, E->grid_cells ? 4 * (E->grid_cells + 1) : 0},
-            {s.grid_site, s0.grid_site, 4 * E->grid_pairs},
-            {s.adj_off, s0.adj_off, E->has_adj ? 8 * (S + 1) : 0}, {s.adj, s0.adj, 4 * E->n_adj}};
-        for (auto& c : cp)
-            if (c.n && cudaMemcpyPeerAsync(c.dst, s.dev, c.src, s0.dev, c.n, s.stream) != cudaSuccess) {
-                set_err("p2m_engine_create: peer copy failed");
-                return fail(P2M_ERR_CUDA);
-            }
-    }
-    for (auto& s : E->slots) {
-        cudaSetDevice(s->dev);
-        if (cudaStreamSynchronize(s->stream) != cudaSuccess) { set_err("p2m_engine_create: replica sync failed"); return fail(P2M_ERR_CUDA); }
-    }
-    E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    for (auto& s : E->slots) {
-        s->params = P;
-        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.lbr = s->lbr; s->params.off = s->off; s->params.lf = s->lf;
-        s->params.lfs = s->lfs; s->params.csph = s->csph; s->params.coff = s->coff;
-        s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
-        s->params.site_pos = s->site_pos;
-        s->params.site_ref = s->site_ref;
-        s->params.grid_off = E->grid_cells ? s->grid_off : nullptr;
-        s->params.grid_site = s->grid_site;
-        s->params.nns = P2M_NNS_GRID;
-        s->params.tile_order = -1;
-        s->params.small_chunks = 2;  // measured on c2 (1, 2 > 4) and c5 (2 ~ 4 > 0)
-        if (const char* v = std::getenv("P2M_SMALL_CHUNKS")) s->params.small_chunks = (uint32_t)std::min(4, std::max(0, std::atoi(v)));
-        if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
-        s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
-        s->params.adj = s->adj;
-    }
-    if (const char* v = std::getenv("P2M_MORTON_BITS")) E->morton_bits = std::min(30, std::max(3, std::atoi(v)));
-    if (const char* v = std::getenv("P2M_E2E_SCHED")) {
-        double x[4];
-        if (std::sscanf(v, "%lf,%lf,%lf,%lf", &x[0], &x[1], &x[2], &x[3]) == 4 && x[0] > 0 && x[1] >= 1 && x[2] > 0 &&
-            x[3] >= 0 && x[3] < 1)
-            for (int k = 0; k < 4; ++k) E->e2e_sched[k] = x[k];
-    }
-    if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(0, std::atoi(v));
-    {
-        int rc = mark_heavy_sites(E.get(), d);
+        int rc = upload_engine(E.get(), P, I, n_devices, device_ids, ndev);
+        if (rc != P2M_OK) return fail(rc);
+        rc = mark_heavy_sites(E.get(), d->site_xyz, d->site_kind);
         if (rc != P2M_OK) return fail(rc);
     }
+    *out = E.release();
+    return P2M_OK;
+}
+
+// ---- device image file "P2MD" (p2m_engine_save / p2m_engine_load) ---------------------------------
+// Little-endian.  magic "P2MD", u32 version, then the engine counts (u64 each), the kernel parameters
+// field by field (fixed widths), then every array of the Image as (u64 byte count, bytes) in a fixed
+// order, then an FNV-1a 64 checksum of everything before it.  Load validates counts, sizes, CSR
+// monotonicity and every stored id against its range before anything reaches a device.
+namespace {
+
+constexpr uint32_t kImageVersion = 1;
+
+struct Fnv {
+    uint64_t h = 1469598103934665603ull;
+    void add(const void* p, size_t n) {
+        const unsigned char* c = (const unsigned char*)p;
+        for (size_t i = 0; i < n; ++i) { h ^= c[i]; h *= 1099511628211ull; }
+    }
+};
+
+struct Writer {
+    FILE* fp;
+    Fnv fnv;
+    bool ok = true;
+    void put(const void* p, size_t n) {
+        if (!ok || !n) return;
+        fnv.add(p, n);
+        ok = std::fwrite(p, 1, n, fp) == n;
+    }
+    template <class T> void v(T x) { put(&x, sizeof x); }
+};
+
+struct Reader {
+    FILE* fp;
+    Fnv fnv;
+    bool ok = true;
+    void get(void* p, size_t n) {
+        if (!ok || !n) return;
+        ok = std::fread(p, 1, n, fp) == n;
+        if (ok) fnv.add(p, n);
+    }
+    template <class T> T v() { T x{}; get(&x, sizeof x); return x; }
+};
+
+// the scalar fields of Params that describe the layout (pointers are re-derived on upload)
+template <class IO, class F>
+void params_fields(Params& P, F&& f) {
+    for (int c = 0; c < 3; ++c) { f(P.dmin[c]); f(P.dmax[c]); f(P.key_lo[c]); f(P.key_scale[c]); f(P.grid_lo[c]); f(P.grid_inv[c]); f(P.grid_res[c]); }
+    f(P.prune_eps); f(P.f32_delta); f(P.lb_margin); f(P.long_tile); f(P.no_seed); f(P.no_batch); f(P.n_nodes); f(P.n_faces);
+}
+
+template <class T>
+bool all_below(const T* p, uint64_t n, uint64_t lim) {
+    for (uint64_t i = 0; i < n; ++i) if ((uint64_t)p[i] >= lim) return false;
+    return true;
+}
+template <class T>
+bool csr_ok(const T* off, uint64_t n, uint64_t total) {
+    if (off[0] != 0 || (uint64_t)off[n] != total) return false;
+    for (uint64_t i = 0; i < n; ++i) if (off[i] > off[i + 1]) return false;
+    return true;
+}
+
+}  // namespace
+
+P2M_API int p2m_engine_save(const p2m_engine* e, const char* path) {
+    if (!e || e->slots.empty()) { set_err("p2m_engine_save: engine not built"); return P2M_ERR_NOT_BUILT; }
+    if (!path) { set_err("p2m_engine_save: null path"); return P2M_ERR_INVALID; }
+    const Slot& s = *e->slots[0];
+    const uint64_t S = e->n_sites, F = e->n_faces, L = e->n_entries;
+    CK(cudaSetDevice(s.dev));
+    CK(cudaDeviceSynchronize());
+    struct A { const void* dev; uint64_t bytes; };
+    const A arrs[] = {
+        {s.kd, 32 * S}, {s.rec, 128 * F}, {s.f32, 16 * F}, {s.bsph, 16 * e->n_batches}, {s.boff, 8 * (S + 1)},
+        {s.lbr, 16ull * kLbRec * F}, {s.off, 8 * (S + 1)}, {s.lf, 4 * L}, {s.lfs, 4 * L}, {s.csph, 16 * e->n_chunks},
+        {s.coff, 8 * (S + 1)}, {s.bvh, 64 * e->n_bvh}, {s.bvh_perm, 4 * F}, {s.site_pos, 32 * S}, {s.site_ref, 32 * S},
+        {s.adj_off, e->has_adj ? 8 * (S + 1) : 0}, {s.adj, e->has_adj ? 4 * e->n_adj : 0},
+        {s.grid_off, e->grid_cells ? 4 * (e->grid_cells + 1) : 0}, {s.grid_site, e->grid_cells ? 4 * e->grid_pairs : 0},
+        {s.heavy, S}};
+    FILE* fp = std::fopen(path, "wb");
+    if (!fp) { set_err(std::string("p2m_engine_save: cannot open ") + path); return P2M_ERR_IO; }
+    Writer w{fp};
+    w.put("P2MD", 4);
+    w.v<uint32_t>(kImageVersion);
+    const uint64_t counts[12] = {S, F, L, e->n_batches, e->n_chunks, e->n_bvh, e->grid_cells, e->grid_pairs,
+                                 (uint64_t)e->has_adj, e->n_adj, e->n_heavy, 0};
+    for (uint64_t c : counts) w.v<uint64_t>(c);
+    Params P = s.params;
+    params_fields<Writer>(P, [&](auto& x) { w.v(x); });
+    std::vector<unsigned char> buf;
+    for (const A& a : arrs) {
+        w.v<uint64_t>(a.bytes);
+        if (!a.bytes) continue;
+        buf.resize(a.bytes);
+        if (cudaMemcpy(buf.data(), a.dev, a.bytes, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            std::fclose(fp);
+            set_err("p2m_engine_save: device read failed");
+            return P2M_ERR_CUDA;
+        }
+        w.put(buf.data(), a.bytes);
+    }
+    const uint64_t sum = w.fnv.h;
+    w.ok = w.ok && std::fwrite(&sum, 8, 1, fp) == 1;
+    const bool ok = w.ok && std::fclose(fp) == 0;
+    if (!ok) { set_err("p2m_engine_save: write failed"); return P2M_ERR_IO; }
+    return P2M_OK;
+}
+
+P2M_API int p2m_engine_load(const char* path, int n_devices, const int* device_ids, p2m_engine** out) {
+    if (!path || !out || n_devices < 1) { set_err("p2m_engine_load: invalid argument"); return P2M_ERR_INVALID; }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        set_err("p2m_engine_load: no CUDA device available");
+        return P2M_ERR_CUDA;
+    }
+    FILE* fp = std::fopen(path, "rb");
+    if (!fp) { set_err(std::string("p2m_engine_load: cannot open ") + path); return P2M_ERR_IO; }
+    Reader r{fp};
+    auto bad = [&](const char* why) { std::fclose(fp); set_err(std::string("p2m_engine_load: ") + why); return (int)P2M_ERR_IO; };
+    char magic[4] = {0, 0, 0, 0};
+    r.get(magic, 4);
+    if (!r.ok || std::memcmp(magic, "P2MD", 4) != 0) return bad("not a device image (magic)");
+    if (r.v<uint32_t>() != kImageVersion || !r.ok) return bad("device image version mismatch");
+    uint64_t c[12];
+    for (auto& x : c) x = r.v<uint64_t>();
+    if (!r.ok) return bad("truncated (header)");
+    auto E = std::make_unique<p2m_engine>();
+    E->n_sites = c[0]; E->n_faces = c[1]; E->n_entries = c[2]; E->n_batches = c[3]; E->n_chunks = c[4];
+    E->n_bvh = c[5]; E->grid_cells = c[6]; E->grid_pairs = c[7]; E->has_adj = c[8] != 0; E->n_adj = c[9];
+    E->n_heavy = c[10];
+    const uint64_t S = c[0], F = c[1], L = c[2];
+    if (S == 0 || F == 0 || S >= (1ull << 32) || F >= (1ull << 32) || L >= (1ull << 40) || c[3] > L + S ||
+        c[4] > L + S || c[5] == 0 || c[5] > 4 * F || c[6] > (1ull << 30) || c[7] >= (1ull << 36) || c[8] > 1 ||
+        c[9] >= (1ull << 36) || c[10] > S)
+        return bad("implausible counts");
+    Params P{};
+    params_fields<Reader>(P, [&](auto& x) { x = r.v<std::remove_reference_t<decltype(x)>>(); });
+    if (!r.ok) return bad("truncated (parameters)");
+    if (P.n_nodes != S || P.n_faces != F) return bad("parameters do not match the counts");
+    Image I;
+    bool sizes_ok = true;
+    auto rd = [&](auto& arr, uint64_t n) {
+        using T = typename std::remove_reference_t<decltype(arr.own)>::value_type;
+        const uint64_t bytes = r.v<uint64_t>();
+        if (!r.ok || bytes != sizeof(T) * n) { sizes_ok = false; return; }
+        std::vector<T> v(n);
+        r.get(v.data(), bytes);
+        arr.take(std::move(v));
+    };
+    rd(I.kd, S); rd(I.rec, 4 * F); rd(I.f32, F); rd(I.bsph, E->n_batches); rd(I.boff, S + 1);
+    rd(I.lbr, (uint64_t)kLbRec * F); rd(I.off, S + 1); rd(I.lf, L); rd(I.lfs, L); rd(I.csph, E->n_chunks);
+    rd(I.coff, S + 1); rd(I.bvh, 2 * E->n_bvh); rd(I.bvh_perm, F); rd(I.site_pos, S); rd(I.site_ref, S);
+    rd(I.adj_off, E->has_adj ? S + 1 : 0); rd(I.adj, E->has_adj ? E->n_adj : 0);
+    rd(I.grid_off, E->grid_cells ? E->grid_cells + 1 : 0); rd(I.grid_site, E->grid_cells ? E->grid_pairs : 0);
+    rd(I.heavy, S);
+    if (!sizes_ok || !r.ok) return bad("truncated or inconsistent array sizes");
+    uint64_t sum = 0;
+    if (std::fread(&sum, 8, 1, fp) != 1 || sum != r.fnv.h) return bad("checksum mismatch (corrupt file)");
+    std::fclose(fp);
+    // ranges of every stored id / offset (a corrupt or foreign file must not reach the kernels)
+    auto inval = [&](const char* why) { set_err(std::string("p2m_engine_load: invalid image: ") + why); return (int)P2M_ERR_IO; };
+    if (!csr_ok(I.off.p, S, L)) return inval("list offsets");
+    if (!all_below(I.lf.p, L, F) || !all_below(I.lfs.p, L, F)) return inval("list face ids");
+    if (!csr_ok(I.boff.p, S, E->n_batches) || !csr_ok(I.coff.p, S, E->n_chunks)) return inval("group offsets");
+    for (uint64_t i = 0; i < S; ++i) {
+        const uint64_t len = I.off.p[i + 1] - I.off.p[i];
+        if (I.boff.p[i + 1] - I.boff.p[i] != (len + 31) / 32 || I.coff.p[i + 1] - I.coff.p[i] != (len + kListChunk - 1) / kListChunk)
+            return inval("group offsets do not match the lists");
+    }
+    for (uint64_t k = 0; k < S; ++k) {
+        uint64_t meta;
+        std::memcpy(&meta, &I.kd.p[k].w, 8);
+        if ((meta & 0xffffffffull) >= S || ((meta >> 32) & 3) > 2) return inval("k-d nodes");
+    }
+    if (!all_below(I.bvh_perm.p, F, F)) return inval("bvh leaf ids");
+    for (uint64_t k = 0; k < E->n_bvh; ++k) {
+        uint64_t meta;
+        std::memcpy(&meta, &I.bvh.p[2 * k + 1].z, 8);
+        const uint64_t cnt = meta >> 32, first = meta & 0xffffffffull;
+        if (cnt ? (first + cnt > F || cnt > 4) : (first == 0 || first >= E->n_bvh)) return inval("bvh nodes");
+    }
+    if (E->has_adj && (!csr_ok(I.adj_off.p, S, E->n_adj) || !all_below(I.adj.p, E->n_adj, S))) return inval("adjacency");
+    if (E->grid_cells) {
+        if (!csr_ok(I.grid_off.p, E->grid_cells, E->grid_pairs) || !all_below(I.grid_site.p, E->grid_pairs, S))
+            return inval("cell-locate grid");
+        if ((uint64_t)P.grid_res[0] * P.grid_res[1] * P.grid_res[2] != E->grid_cells) return inval("grid resolution");
+    }
+    if (!all_below(I.heavy.p, S, 2)) return inval("heavy flags");
+    auto fail = [&](int rc) { for (auto& x : E->slots) free_slot(*x); return rc; };
+    int rc = upload_engine(E.get(), P, I, n_devices, device_ids, ndev);
+    if (rc != P2M_OK) return fail(rc);
     *out = E.release();
     return P2M_OK;
 }

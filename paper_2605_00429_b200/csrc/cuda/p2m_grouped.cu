@@ -226,17 +226,6 @@ static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 
 constexpr int kWarps = kTile / 32;
 
-#ifndef P2M_COMPACT
-#define P2M_COMPACT 1   // rare path: compacted (row, candidate) pass pairs, 32 per round (0: union walk)
-#endif
-// Per-warp shared scratch of the compacted rare path: the batch's (row lane, candidate) pass pairs and
-// the per-row lexicographic (d^2 bits, face id) minimum of the round's exact evaluations.
-struct RowScratch {
-    uint16_t pl[32 * 32];
-    unsigned long long bk[32];
-    uint32_t bf[32];
-    uint32_t ex[32];
-};
 
 // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)}, lb: 32 x
 // 64-byte lower-bound records, fid: 32 face ids), scanned for this lane's row.  Each lane computes a
@@ -252,7 +241,7 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
                                                uint32_t& exact, unsigned long long& passes,
                                                unsigned long long& rare_iters, unsigned long long& sbytes,
                                                const float4* pair, float4* lb, const uint32_t* fid, int valid,
-                                               bool stage_lb, uint32_t my_f, int lane, RowScratch& rs) {
+                                               bool stage_lb, uint32_t my_f, int lane) {
     const float K = 1.000001f;
     const float delta = p.f32_delta;
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
@@ -295,90 +284,6 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         }
         __syncwarp();
     }
-#if P2M_COMPACT
-    if (!um) return;
-    // Compact the warp's (row lane, candidate) pairs that passed the sphere filter and test them 32 at
-    // a time, one pair per lane: every lane works in every round, instead of walking the union of the
-    // rows' masks with only the lanes whose bit is set busy (c5: 38% of the lane slots).
-    const uint32_t cnt = __popc(mask);
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    {
-        uint32_t wpos = incl - cnt, m = mask;
-        while (m) {
-            const int k = __ffs(m) - 1;
-            m &= m - 1;
-            rs.pl[wpos++] = (uint16_t)(lane << 5 | k);
-        }
-    }
-    if (kCounters) rs.ex[lane] = 0u;
-    // squared threshold of the tight bound, from the row's CURRENT d_min (refreshed after each round)
-    auto th2_of = [&](uint64_t dk) {
-        float dkx, dky;
-        upk2(dk, dkx, dky);
-        const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-        return __fmul_ru(thl, thl);
-    };
-    float th2 = th2_of(DK);
-    __syncwarp();
-    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
-        const uint32_t t = t0 + lane;
-        const bool has = t < total;
-        const uint32_t pr = has ? rs.pl[t] : 0u;
-        const int r = (int)(pr >> 5), k = (int)(pr & 31u);
-        const float qx = __shfl_sync(0xffffffffu, qxf, r), qy = __shfl_sync(0xffffffffu, qyf, r),
-                    qz = __shfl_sync(0xffffffffu, qzf, r), thr = __shfl_sync(0xffffffffu, th2, r);
-        bool sv = false;
-        if (has) {
-            const float4* rec = lb + kLbRec * k;
-            sv = !(lb2_plane(rec, qx, qy, qz) > thr) && !(lb2_vert(rec, qx, qy, qz) > thr);
-        }
-        if (!__any_sync(0xffffffffu, sv)) continue;
-        // exact fp64 evaluation of the surviving pairs, in parallel (REF geom.cpp:31-70)
-        const V qr{__shfl_sync(0xffffffffu, q.x, r), __shfl_sync(0xffffffffu, q.y, r), __shfl_sync(0xffffffffu, q.z, r)};
-        unsigned long long key = 0;
-        uint32_t f = 0;
-        if (sv) {
-            f = fid[k];
-            V a, bb3, c3, pp3;
-            load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);
-            key = (unsigned long long)__double_as_longlong(closest_tri(qr, a, bb3, c3, &pp3));  // d^2 >= +0
-        }
-        if (kCounters && lane == 0) sbytes += 96ull * __popc(__ballot_sync(0xffffffffu, sv));
-        // per-row lexicographic (d^2, face id) min over the row's current best and its survivors:
-        // d^2 >= +0, so its bit pattern orders like its value
-        const unsigned long long old = (unsigned long long)__double_as_longlong(best);
-        rs.bk[lane] = old;
-        rs.bf[lane] = bf;
-        __syncwarp();
-        if (sv) atomicMin(&rs.bk[r], key);
-        __syncwarp();
-        const unsigned long long nk = rs.bk[lane];
-        if (nk != old) rs.bf[lane] = 0xffffffffu;  // a strictly smaller d^2: its face ids only
-        __syncwarp();
-        if (sv && key == rs.bk[r]) atomicMin(&rs.bf[r], f);
-        if (kCounters && sv) atomicAdd(&rs.ex[r], 1u);
-        __syncwarp();
-        if (active) {
-            bf = rs.bf[lane];
-            if (nk != old) {
-                best = __longlong_as_double((long long)nk);
-                // any upper bound of sqrt(best) is a valid d_min for the prunes: the fp32 sqrt rounded up
-                // of best rounded up (cheaper than the fp64 sqrt)
-                const float dkf = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(best)), delta), K);
-                DK = pk2(dkf, dkf);
-                th2 = th2_of(DK);
-            }
-        }
-        __syncwarp();
-    }
-    if (kCounters) exact += rs.ex[lane];
-#else
     // the exact test of one candidate kk of this lane: the tight lower bound against the CURRENT
     // d_min (the batch mask used the d_min of the batch start), then fp64
     auto visit = [&](int kk) -> bool {
@@ -414,7 +319,6 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         if (kCounters && __any_sync(0xffffffffu, ex) && lane == 0) sbytes += 96;  // one face record per warp visit
     }
 
-#endif
 }
 
 // d_min seeds of one row of site s (both are upper bounds of the distance to the mesh, so the
@@ -495,8 +399,6 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     __shared__ float4 s_pair[kWarps][32];
     __shared__ uint32_t s_fid[kWarps][32];
     __shared__ float4 s_lb[kWarps][32 * kLbRec];
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    RowScratch* s_rs = reinterpret_cast<RowScratch*>(s_dyn);  // kWarps of them (dynamic: > 48 KB total)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t nt = meta[0], ns = meta[2];
     const uint32_t ti = blockIdx.x * kWarps + w;
@@ -602,7 +504,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
             __syncwarp();
             if (kCounters && lane == 0) sbytes += 20ull * valid;  // staged ids + fp32 records
             scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      wp, wl, wf, valid, true, f, lane, s_rs[w]);
+                                      wp, wl, wf, valid, true, f, lane);
             __syncwarp();                        // the slice is rewritten by the next batch
         }
     }
@@ -667,8 +569,6 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
     __shared__ uint32_t s_fid[kChunk];
     __shared__ float4 s_lb[kChunk * kLbRec];     // the chunk's fp32 lower-bound records (96 B each)
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    RowScratch* s_rs = reinterpret_cast<RowScratch*>(s_dyn);  // per-warp rare-path scratch (dynamic)
     __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
     __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
     __shared__ uint32_t s_cw[kWinChunks / 32];   // chunks of the current window some row must scan
@@ -840,7 +740,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
                               uint32_t my_f) {
             scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      pair, lb, fid, valid, stage_lb, my_f, lane, s_rs[w]);
+                                      pair, lb, fid, valid, stage_lb, my_f, lane);
         };
         if (G == 1) {
             // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
@@ -1229,26 +1129,17 @@ cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* 
     const unsigned g = (unsigned)max_tiles(n, p.n_nodes);
     cudaError_t e;
     const bool small = p.small_chunks && side;
-    const size_t dyn = P2M_COMPACT ? sizeof(RowScratch) * kWarps : 0;
-    static bool attr = false;                    // > 48 KB of shared memory per CTA: opt in once
-    if (!attr && dyn) {
-        cudaFuncSetAttribute(k_scan_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaFuncSetAttribute(k_scan_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaFuncSetAttribute(k_scan_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaFuncSetAttribute(k_scan_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        attr = true;
-    }
     if (small) {                                 // fork: small tiles on the side stream
         if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
         const unsigned gs = (g + kWarps - 1) / kWarps;
-        if (counters) k_scan_small<true><<<gs, kTile, dyn, side>>>(p, q, rows, key, tiles, meta, order, o);
-        else k_scan_small<false><<<gs, kTile, dyn, side>>>(p, q, rows, key, tiles, meta, order, o);
+        if (counters) k_scan_small<true><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_small<false><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = cudaEventRecord(join, side)) != cudaSuccess) return e;
     }
-    if (counters) k_scan_tiles<true><<<g, kTile, dyn, s>>>(p, q, rows, key, tiles, meta, order, o);
-    else k_scan_tiles<false><<<g, kTile, dyn, s>>>(p, q, rows, key, tiles, meta, order, o);
+    if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+    else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (small && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;  // join
     return cudaGetLastError();

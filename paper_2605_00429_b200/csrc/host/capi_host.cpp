@@ -169,7 +169,21 @@ P2M_API int p2m_host_closest_point(const p2m_host_engine* he, const double* q, d
 // EngineIndexFile (REF/SPEC.md:588-591): magic "P2MX", LE u32 version, mesh hash, D, sites
 // (kind, position, reference), per-site table offsets + face ids, config echo.  The BVH and the
 // NNS index are rebuilt on load (REF/SPEC.md:639).
-static const uint32_t kFileVersion = 3;  // v2 adds the Voronoi cell boxes, v3 the Delaunay adjacency
+static const uint32_t kFileVersion = 4;  // v2 cell boxes, v3 Delaunay adjacency, v4 field-by-field config/stats
+
+// config and stats field by field with explicit widths (little-endian), never as struct dumps
+template <class IO>
+static void cfg_fields(p2m_build_config& c, IO&& io) {
+    io(c.augment); io(c.alpha); io(c.k); io(c.rho); io(c.max_rounds); io(c.domain_scale); io(c.n_threads);
+    io(c.strict_mesh); io(c.aux_corner_union);
+}
+template <class IO>
+static void stats_fields(p2m_build_stats& t, IO&& io) {
+    io(t.n_input_vertices); io(t.n_input_faces); io(t.n_vertices); io(t.n_faces); io(t.merged_vertices);
+    io(t.removed_faces); io(t.n_sites); io(t.n_aux_sites); io(t.rounds_used); io(t.mean_edge); io(t.tau);
+    io(t.list_entries); io(t.list_max); io(t.list_avg); io(t.t_voronoi_s); io(t.t_augment_s); io(t.t_tables_s);
+    io(t.t_total_s); io(t.cell_corners);
+}
 
 P2M_API int p2m_host_engine_save(const p2m_host_engine* he, const char* path) {
     return guarded([&] {
@@ -184,8 +198,10 @@ P2M_API int p2m_host_engine_save(const p2m_host_engine* he, const char* path) {
         w(&h.mesh_hash, 8);
         double dom[6] = {h.D.lo.x, h.D.lo.y, h.D.lo.z, h.D.hi.x, h.D.hi.y, h.D.hi.z};
         w(dom, sizeof dom);
-        w(&h.cfg, sizeof h.cfg);
-        w(&h.stats, sizeof h.stats);
+        p2m_build_config cfg = h.cfg;
+        p2m_build_stats st = h.stats;
+        cfg_fields(cfg, [&](auto& x) { w(&x, sizeof x); });
+        stats_fields(st, [&](auto& x) { w(&x, sizeof x); });
         uint64_t S = h.sites.size();
         w(&S, 8);
         w(h.kind.data(), S);
@@ -226,9 +242,14 @@ P2M_API int p2m_host_engine_load(const char* path, const double* vertices, uint6
         r(&hash, 8);
         double dom[6];
         r(dom, sizeof dom);
-        r(&h.cfg, sizeof h.cfg);
-        r(&h.stats, sizeof h.stats);
+        h.cfg = p2m_build_config{};
+        h.stats = p2m_build_stats{};
+        cfg_fields(h.cfg, [&](auto& x) { r(&x, sizeof x); });
+        stats_fields(h.stats, [&](auto& x) { r(&x, sizeof x); });
         if (!ok) { std::fclose(fp); set_error("EngineIndexFile truncated (header)"); return (int)P2M_ERR_IO; }
+        if (!(h.cfg.alpha > 0) || h.cfg.k < 1 || !(h.cfg.rho > 0) || h.cfg.max_rounds < 1 || !(h.cfg.domain_scale >= 1)) {
+            std::fclose(fp); set_error("EngineIndexFile corrupt (config)"); return (int)P2M_ERR_IO;
+        }
         // re-validate the caller's mesh exactly as the build did and compare the hash
         p2m_build_config c = h.cfg;
         auto probe = p2m::build_engine_mesh_only(vertices, n_vertices, faces, n_faces, c);
@@ -272,6 +293,24 @@ P2M_API int p2m_host_engine_load(const char* path, const double* vertices, uint6
         r(tail, 4);
         std::fclose(fp);
         if (!ok || std::memcmp(tail, "XM2P", 4) != 0) { set_error("EngineIndexFile truncated"); return (int)P2M_ERR_IO; }
+        // contents: every id and offset within range before anything uses them (a corrupt or foreign
+        // file must fail here, not read out of bounds in the table or query paths)
+        const uint64_t NF = h.F.size() / 3;
+        auto corrupt = [&](const char* what) { set_error(std::string("EngineIndexFile corrupt (") + what + ")"); return (int)P2M_ERR_IO; };
+        if (h.off[0] != 0) return corrupt("table offsets");
+        for (uint64_t i = 0; i < S; ++i) if (h.off[i] > h.off[i + 1]) return corrupt("table offsets");
+        for (uint32_t f : h.lists) if (f >= NF) return corrupt("face ids");
+        for (uint64_t i = 0; i < S; ++i) if (h.adj_off[i] > h.adj_off[i + 1]) return corrupt("adjacency offsets");
+        for (uint32_t a : h.adj) if (a >= S) return corrupt("adjacency ids");
+        uint64_t n_sent = 0;
+        for (uint64_t i = 0; i < S; ++i) {
+            if (h.kind[i] > 2) return corrupt("site kinds");
+            if (!std::isfinite(h.site_xyz[3 * i]) || !std::isfinite(h.site_xyz[3 * i + 1]) || !std::isfinite(h.site_xyz[3 * i + 2]))
+                return corrupt("site positions");
+            n_sent += h.kind[i] == 1;
+        }
+        for (uint32_t id : h.sentinel_ids) if (id >= S || h.kind[id] != 1) return corrupt("sentinel ids");
+        if (n_sent != sizeof h.sentinel_ids / sizeof h.sentinel_ids[0]) return corrupt("sentinel count");
         h.sites.resize(S);
         for (uint64_t i = 0; i < S; ++i) h.sites[i] = p2m::ld3(&h.site_xyz[3 * i]);
         h.bvh.build(h.tri.data(), h.F.size() / 3, 4);

@@ -266,6 +266,23 @@ class Engine:
         self.devices = tuple(devices)
         return self
 
+    @classmethod
+    def load(cls, path: str, devices: Sequence[int] = (0,)) -> "Engine":
+        """An engine straight from a device image file (p2m_engine_load): no host engine, no
+        re-packing; bit-identical queries to the engine that was saved."""
+        self = cls.__new__(cls)
+        self.host_engine = None
+        ids = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        L.check(L.cuda().p2m_engine_load(path.encode(), len(devices), ids, C.byref(h)))
+        self._h = h
+        self.devices = tuple(devices)
+        return self
+
+    def save(self, path: str) -> None:
+        """Write the packed device layout (p2m_engine_save, "P2MD" v1)."""
+        L.check(L.cuda().p2m_engine_save(self.handle, path.encode()))
+
     def close(self):
         h = getattr(self, "_h", None)
         if h:

@@ -234,6 +234,33 @@ def test_save_load_round_trip(ico3):
             P.HostEngine.load(path, V, F)  # truncated
 
 
+def test_load_rejects_corrupt_contents(ico3, tmp_path):
+    """EngineIndexFile v4: config/stats are stored field by field, and load checks every
+    id and offset against its range -- a face id >= F, a bad site kind or non-monotone offsets fail
+    with P2M_ERR_IO instead of reaching the table or query paths."""
+    V, F, h = ico3
+    path = str(tmp_path / "e.p2mx")
+    h.save(path)
+    blob = bytearray(open(path, "rb").read())
+    a = h.arrays()
+    S = len(a["site_kind"])
+    head = 4 + 4 + 8 + 48 + (6 * 4 + 3 * 8) + (8 * 8 + 4 + 2 * 8 + 2 * 8 + 8 + 4 * 8 + 8) + 8
+    kind_at = head
+    off_at = head + S + 48 * S + 32
+    lists_at = off_at + 8 * (S + 1)
+    assert bytes(blob[kind_at:kind_at + S]) == a["site_kind"].tobytes()
+    assert bytes(blob[lists_at:lists_at + 8]) == a["list_faces"][:2].tobytes()
+    for name, at, val in (("face ids", lists_at, b"\xff\xff\xff\xff"), ("site kinds", kind_at + 3, b"\x07"),
+                          ("table offsets", off_at + 8 * 5, b"\x00" * 8)):
+        bad = bytearray(blob)
+        bad[at:at + len(val)] = val
+        p2 = str(tmp_path / "bad.p2mx")
+        open(p2, "wb").write(bytes(bad))
+        with pytest.raises(P.P2MError, match="corrupt") as ei:
+            P.HostEngine.load(p2, V, F)
+        assert ei.value.code == -6 and name.split()[0] in str(ei.value), name
+
+
 def test_config_meshes_and_queries():
     V, F = P.mesh_config(1)
     assert (len(V), len(F)) == (10242, 20480)

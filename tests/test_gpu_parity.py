@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from conftest import big_config, oracle_checker
 import paper_2605_00429_b200 as P
 from paper_2605_00429_b200 import _lib as L
 
@@ -54,7 +55,7 @@ def test_parity_vs_oracle(request, fixture, nq, cfg):
         q = P.gen_queries(cfg, V, F, 0, nq)
     eng = P.Engine(h)
     r = eng.batch_query(q)
-    ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
+    ref = oracle_checker(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
     _compare(r, ref, nq)
     _check_counters(r, ref, sequential=False)
 
@@ -67,7 +68,7 @@ def test_scan_modes_identical(c2, mode):
     eng = P.Engine(h)
     L.check(L.cuda().p2m_set_scan_mode(eng.handle, mode))
     r = eng.batch_query(q)
-    ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
+    ref = oracle_checker(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
     _compare(r, ref, len(q))
     _check_counters(r, ref, sequential=(mode == 1))
 
@@ -125,7 +126,7 @@ def test_tiny_meshes(mesh):
     h = P.HostEngine.build(V, F)
     q = np.random.default_rng(1).uniform(-3, 3, size=(5000, 3))
     r = P.Engine(h).batch_query(q)
-    ref = O.OracleEngine(h.arrays()).batch_query(q)
+    ref = oracle_checker(h.arrays()).batch_query(q)
     _compare(r, ref, len(q))
 
 
@@ -144,7 +145,7 @@ def test_nearest_site_and_per_query_counters(c1):
     L.check(L.cuda().p2m_query_device_counters(eng.handle, 0, C.c_void_p(dq.data_ptr()), len(q),
                                                C.c_void_p(pq.data_ptr()), s))
     torch.cuda.synchronize()
-    ref = O.OracleEngine(h.arrays()).batch_query(q, per_query=True)
+    ref = oracle_checker(h.arrays()).batch_query(q, per_query=True)
     assert np.array_equal(site.cpu().numpy().astype(np.uint32), ref["site"])
     pq = pq.cpu().numpy()
     assert np.array_equal(pq[:, 0], ref["per_query"][:, 0])
@@ -195,15 +196,36 @@ def test_kernel_launch_count(ico3):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", [3, 4, 5])
-def test_parity_large_configs(cfg):
-    V, F = P.mesh_config(cfg)
-    h = P.HostEngine.build(V, F)
-    q = P.gen_queries(cfg, V, F, 0, 200_000)
+@pytest.mark.parametrize("cfg,nq", [(3, 1_000_000), (4, 1_000_000), (5, 2_000_000)])
+def test_parity_large_configs(cfg, nq):
+    """c3..c5 through the public host API, every row bit-identical to the reference CPU query path
+    (oracle/_ref) -- 2 M rows on c5, the benchmark config."""
+    V, F, h = big_config(cfg)
+    q = P.gen_queries(cfg, V, F, 0, nq)
     r = P.Engine(h).batch_query(q)
-    ref = O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
+    ref = oracle_checker(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE)
     _compare(r, ref, len(q))
     _check_counters(r, ref, sequential=False)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_exact_vs_brute_force(cfg, c2):
+    """Acceptance (REF/SPEC.md:508, 665-667): on a 10^4-query sample of each benchmark config the
+    GPU answer equals brute_force_closest over ALL faces (REF/SPEC.md:536-544) -- the check that
+    does not trust the interception tables at all.  Distance and closest point bit-identical; the
+    face id may differ only on an exact tie of d^2 (never observed: the tables keep every tie)."""
+    V, F, h = c2 if cfg == 2 else big_config(cfg)
+    q = P.gen_queries(cfg, V, F, 3_000_000, 10_000)
+    r = P.Engine(h).batch_query(q)
+    tri = h.arrays()["tri"].reshape(-1, 9)
+    bf = O.batch_brute_force(tri, q, reference=O.have_reference())
+    same_face = r.face == bf["face"]
+    d2 = r.distance * r.distance
+    assert r.distance.tobytes() == np.sqrt(bf["d2"]).tobytes()
+    assert np.all(same_face | (bf["d2"] == d2)), f"{(~same_face).sum()} rows differ"
+    assert r.closest[same_face].tobytes() == bf["closest"][same_face].tobytes()
+    assert (~same_face).sum() == 0
 
 
 def test_grid_and_kdtree_locate_agree(c2):
@@ -221,7 +243,7 @@ def test_grid_and_kdtree_locate_agree(c2):
         del os.environ["P2M_NO_GRID"]
     for k in ("distance", "closest", "face", "site", "flags"):
         assert getattr(r_grid, k).tobytes() == getattr(r_kd, k).tobytes(), k
-    ref = O.OracleEngine(h.arrays()).batch_query(q)
+    ref = oracle_checker(h.arrays()).batch_query(q)
     _compare(r_grid, ref, len(q))
 
 
@@ -260,7 +282,7 @@ def test_fp32_prefilters_stress(variant):
         Vv.mean(0) + rng.uniform(-1.3, 1.3, size=(40_000, 3)) * scale,
     ])
     r = P.Engine(h).batch_query(q)
-    ref = O.OracleEngine(h.arrays()).batch_query(q)
+    ref = oracle_checker(h.arrays()).batch_query(q)
     _compare(r, ref, len(q))
 
 
@@ -315,7 +337,7 @@ def test_scan_schedules_identical(c2, env, monkeypatch):
            "closest": base.closest}
     _compare(r, ref, len(q))
     if env == {"P2M_SMALL_CHUNKS": "4"}:
-        _compare(r, O.OracleEngine(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE), len(q))
+        _compare(r, oracle_checker(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE), len(q))
 
 
 def test_concurrent_device_calls_one_engine(c2):
@@ -436,3 +458,33 @@ def test_table_miss_falls_back_exactly(ico3):
     # the fallback answer is the exact one, so it equals the superset engine's row
     assert r.distance.tobytes() == base.distance.tobytes() and np.array_equal(r.face, base.face)
     assert np.array_equal(r.flags[~hit], base.flags[~hit])
+
+
+def test_device_image_round_trip(c2, tmp_path):
+    """the engine saved as its packed device layout and loaded straight into
+    it (no host engine, no re-packing) answers bit-identically to the oracle and to the engine that
+    was saved (REF/SPEC.md:588-591: round trip gives identical query results); corrupt and truncated
+    files fail with P2M_ERR_IO before anything reaches the device."""
+    V, F, h = c2
+    q = P.gen_queries(2, V, F, 5_000_000, 300_000)
+    eng = P.Engine(h)
+    path = str(tmp_path / "c2.p2md")
+    eng.save(path)
+    loaded = P.Engine.load(path)
+    r0, r1 = eng.batch_query(q), loaded.batch_query(q)
+    for k in ("distance", "closest", "face", "site", "flags"):
+        assert getattr(r0, k).tobytes() == getattr(r1, k).tobytes(), k
+    _compare(r1, oracle_checker(h.arrays()).batch_query(q, prune=O.PRUNE_SAFE), len(q))
+    assert loaded.info()["device_bytes"] == eng.info()["device_bytes"]
+    blob = open(path, "rb").read()
+    for name, data in (("trunc", blob[: len(blob) // 2]), ("flip", blob[:200] + bytes([blob[200] ^ 1]) + blob[201:]),
+                       ("magic", b"XXXX" + blob[4:])):
+        bad = str(tmp_path / f"{name}.p2md")
+        open(bad, "wb").write(data)
+        with pytest.raises(L.P2MError) as ei:
+            P.Engine.load(bad)
+        assert ei.value.code == -6, name
+    # replicated on two slots from the image (same GPU twice: the peer-copy path)
+    two = P.Engine.load(path, devices=[0, 0])
+    r2 = two.batch_query(q)
+    assert r2.distance.tobytes() == r0.distance.tobytes() and np.array_equal(r2.face, r0.face)

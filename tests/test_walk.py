@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from conftest import oracle_checker
 import paper_2605_00429_b200 as P
 
 
@@ -104,7 +105,7 @@ def test_gpu_strategy_neutrality(request, fixture, cfg):
     for st in ("kdtree", "walk"):
         for k in ("distance", "closest", "face", "site", "flags"):
             assert getattr(res[st], k).tobytes() == getattr(res["grid"], k).tobytes(), (st, k)
-    ref = O.OracleEngine(a).batch_query(q)
+    ref = oracle_checker(a).batch_query(q)
     assert np.array_equal(res["walk"].site, ref["site"])
     assert res["walk"].distance.tobytes() == ref["distance"].tobytes()
 
