@@ -266,6 +266,7 @@ struct Slot {
     uint64_t* adj_off = nullptr;
     uint32_t* adj = nullptr;
     Params params{};
+    std::mutex pmu;  // guards params (p2m_set_nns_strategy) against the snapshot every call takes
     std::mutex mu;
     // host-API path: kPipe streams, each with a chunk-sized staging set, so the H2D copy of one
     // chunk, the kernels of another and the D2H copy of a third overlap
@@ -307,7 +308,7 @@ struct Slot {
     static constexpr int kRing = 256;
     static constexpr int kEv = 6;  // morton | sort | descend | regroup sort | scan | end
     std::vector<cudaEvent_t> ev;   // kEv per ring entry
-    int recorded = 0;
+    std::atomic<int> recorded{0};  // profiling-ring slots claimed (atomic: concurrent device calls)
 };
 
 }  // namespace
@@ -378,8 +379,17 @@ struct Grid {
     std::vector<uint32_t> off, site;
 };
 
-bool build_grid(const p2m_engine_desc* d, const double* key_lo, const double* key_ext, Grid& g) {
-    if (!d->site_cell_box) return false;
+}  // namespace
+namespace p2m { namespace dev {
+bool build_grid_device(int dev, const D4* kd_host, uint32_t S, const double lo[3], const double inv[3],
+                       const uint32_t res[3], std::vector<uint32_t>& off, std::vector<uint32_t>& site);
+} }
+namespace {
+
+// Without cell boxes (an external builder's desc) the same grid is built on device `dev` from the
+// sites alone (p2m_grid.cu: k-d radius search + the affine bisector test at the cell corners).
+bool build_grid(const p2m_engine_desc* d, const double* key_lo, const double* key_ext, Grid& g,
+                const std::vector<D4>& kd, int dev) {
     const uint64_t S = d->n_sites;
     double hi[3], c[3];
     for (int k = 0; k < 3; ++k) { hi[k] = key_lo[k] + key_ext[k]; c[k] = 0.5 * (key_lo[k] + hi[k]); }
@@ -388,8 +398,10 @@ bool build_grid(const p2m_engine_desc* d, const double* key_lo, const double* ke
     for (uint64_t s = 0; s < S; ++s) {
         if (d->site_kind[s] == P2M_SITE_SENTINEL) continue;
         ++n_real;
-        const double* b = d->site_cell_box + 6 * s;
-        for (int k = 0; k < 6; ++k) if (!std::isfinite(b[k])) return false;
+        if (d->site_cell_box) {
+            const double* b = d->site_cell_box + 6 * s;
+            for (int k = 0; k < 6; ++k) if (!std::isfinite(b[k])) return false;
+        }
         const double* p = d->site_xyz + 3 * s;
         const double dd = (p[0] - c[0]) * (p[0] - c[0]) + (p[1] - c[1]) * (p[1] - c[1]) + (p[2] - c[2]) * (p[2] - c[2]);
         if (dd < best) { best = dd; s0 = s; }
@@ -420,6 +432,10 @@ bool build_grid(const p2m_engine_desc* d, const double* key_lo, const double* ke
         g.lo[k] = key_lo[k];
         g.res[k] = (uint32_t)std::min(512.0, std::max(1.0, std::ceil(key_ext[k] / cell)));
         g.inv[k] = (double)g.res[k] / key_ext[k];
+    }
+    if (!d->site_cell_box) {
+        if (std::getenv("P2M_NO_DEVICE_GRID")) return false;
+        return p2m::dev::build_grid_device(dev, kd.data(), (uint32_t)S, g.lo, g.inv, g.res, g.off, g.site);
     }
     double dspan = 0.0;
     for (int k = 0; k < 3; ++k) dspan += (d->domain_max[k] - d->domain_min[k]) * (d->domain_max[k] - d->domain_min[k]);
@@ -578,7 +594,12 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
     // launch order of the scan tiles (P2M_TILE_ORDER): measured on c2, longest-first wins below a
     // few million rows (the heaviest tiles otherwise start last and set the tail) and site order
     // above (neighbouring tiles share lists in L2); -1 = choose by batch size
-    int order = s.params.tile_order;
+    Params sp;
+    {
+        std::lock_guard<std::mutex> lk(s.pmu);
+        sp = s.params;  // one consistent snapshot per call
+    }
+    int order = sp.tile_order;
     if (order < 0) order = n < (4ull << 20) ? 1 : 0;
     const bool lpt = true;  // the launch order array (site order, LPT or buckets; small tiles last) always exists
     uint32_t* tord = nullptr;  // 4 x max_t: keys, sorted keys, tile ids, launch order
@@ -603,10 +624,15 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
             if (lpt) CK(cudaMallocAsync(&tord, 16 * max_t, st));
         }
     }
-    const bool prof = allow_prof && E->profiling && s.recorded < Slot::kRing;
-    cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * s.recorded] : nullptr;
-    if (prof) { CK(cudaEventRecord(ev[0], st)); ++s.recorded; }
-    CK(p2m::dev::launch_morton(d_q, n, s.params, keys, rows, st));
+    int ring = -1;
+    if (allow_prof && E->profiling && s.recorded.load() < Slot::kRing) {
+        ring = s.recorded.fetch_add(1);
+        if (ring >= Slot::kRing) ring = -1;
+    }
+    const bool prof = ring >= 0;
+    cudaEvent_t* ev = prof ? &s.ev[Slot::kEv * ring] : nullptr;
+    if (prof) CK(cudaEventRecord(ev[0], st));
+    CK(p2m::dev::launch_morton(d_q, n, sp, keys, rows, st));
     if (prof) CK(cudaEventRecord(ev[1], st));
     // the Morton order only has to be spatially coherent: sorting on the top morton_bits of the
     // 30-bit key saves radix passes (8 bits per onesweep pass)
@@ -614,25 +640,25 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows, rows2, (int64_t)n, 30 - mbits, 30, st));
     if (prof) CK(cudaEventRecord(ev[2], st));
     if (nearest_only) {
-        CK(p2m::dev::launch_nearest(s.params, d_q, rows2, n, d_site_only, st));
+        CK(p2m::dev::launch_nearest(sp, d_q, rows2, n, d_site_only, st));
         if (prof) for (int k = 3; k < Slot::kEv; ++k) CK(cudaEventRecord(ev[k], st));
     } else if (E->scan_mode == P2M_SCAN_FUSED) {
-        CK(p2m::dev::launch_query(s.params, d_q, rows2, n, o, counters, st));
+        CK(p2m::dev::launch_query(sp, d_q, rows2, n, o, counters, st));
         if (prof) for (int k = 3; k < Slot::kEv; ++k) CK(cudaEventRecord(ev[k], st));
     } else {
         // descend in Morton order (keys buffer reused for the site keys), regroup by site (stable),
         // then scan per site tile
-        CK(p2m::dev::launch_descend(s.params, d_q, rows2, n, keys, o, counters, st));
+        CK(p2m::dev::launch_descend(sp, d_q, rows2, n, keys, o, counters, st));
         if (prof) CK(cudaEventRecord(ev[3], st));
         const int bits = std::max(1, 64 - __builtin_clzll((unsigned long long)E->n_sites));  // keys <= n_sites
         CK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, rows2, rows, (int64_t)n, 0, bits, st));
         // tiles over the site-sorted order (keys / rows2 are free again: hpos / run starts)
-        CK(p2m::dev::launch_tiles(s.params, keys2, n, (uint32_t)E->n_sites, keys, rows2, flag, tix, tiles, meta, tmp, tb, st));
+        CK(p2m::dev::launch_tiles(sp, keys2, n, (uint32_t)E->n_sites, keys, rows2, flag, tix, tiles, meta, tmp, tb, st));
         if (prof) CK(cudaEventRecord(ev[4], st));
         const char* trace_path = std::getenv("P2M_TILE_TRACE");
         unsigned long long* trace = nullptr;
         const uint64_t ntile_max = p2m::dev::max_tiles(n, E->n_sites);
-        Params prm = s.params;
+        Params prm = sp;
         prm.tile_order = order;
         if (trace_path) {  // debug: per-tile timing dump (scripts/tile_trace.py)
             CK(cudaMallocAsync(&trace, 32 * ntile_max, st));
@@ -1089,7 +1115,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     {
         double ext[3];
         for (int c = 0; c < 3; ++c) ext[c] = kext[c];
-        if (build_grid(d, P.key_lo, ext, grid)) {
+        if (build_grid(d, P.key_lo, ext, grid, kd, device_ids ? device_ids[0] : 0)) {
             E->grid_cells = (uint64_t)grid.res[0] * grid.res[1] * grid.res[2];
             E->grid_pairs = grid.site.size();
             for (int c = 0; c < 3; ++c) { P.grid_lo[c] = grid.lo[c]; P.grid_inv[c] = grid.inv[c]; P.grid_res[c] = grid.res[c]; }
@@ -1127,6 +1153,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         if (rc != P2M_OK) return fail(rc);
         rc = mark_heavy_sites(E.get(), d->site_xyz, d->site_kind);
         if (rc != P2M_OK) return fail(rc);
+        E->bytes += S;                           // the heavy-site flags (not part of the packed image)
     }
     *out = E.release();
     return P2M_OK;
@@ -1731,14 +1758,15 @@ P2M_API int p2m_last_timings(p2m_engine* e, int slot, float* ms) {
     Slot& s = *e->slots[slot];
     double acc[Slot::kEv] = {0};
     CK(cudaSetDevice(s.dev));
-    for (int r = 0; r < s.recorded; ++r) {
+    const int nrec = std::min(s.recorded.load(), (int)Slot::kRing);
+    for (int r = 0; r < nrec; ++r) {
         cudaEvent_t* ev = &s.ev[Slot::kEv * r];
         CK(cudaEventSynchronize(ev[Slot::kEv - 1]));
         float m;
         for (int k = 0; k + 1 < Slot::kEv; ++k) { CK(cudaEventElapsedTime(&m, ev[k], ev[k + 1])); acc[k] += m; }
         CK(cudaEventElapsedTime(&m, ev[0], ev[Slot::kEv - 1])); acc[Slot::kEv - 1] += m;
     }
-    for (int k = 0; k < Slot::kEv; ++k) ms[k] = s.recorded ? (float)(acc[k] / s.recorded) : 0.0f;
+    for (int k = 0; k < Slot::kEv; ++k) ms[k] = nrec ? (float)(acc[k] / nrec) : 0.0f;
     s.recorded = 0;
     return P2M_OK;
 }
@@ -1761,7 +1789,7 @@ P2M_API int p2m_set_nns_strategy(p2m_engine* e, int strategy) {
         return P2M_ERR_INVALID;
     }
     for (auto& s : e->slots) {
-        std::lock_guard<std::mutex> lk(s->mu);
+        std::lock_guard<std::mutex> lk(s->pmu);
         s->params.nns = strategy;
     }
     return P2M_OK;

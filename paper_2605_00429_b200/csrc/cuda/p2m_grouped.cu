@@ -241,11 +241,17 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
                                                uint32_t& exact, unsigned long long& passes,
                                                unsigned long long& rare_iters, unsigned long long& sbytes,
                                                const float4* pair, float4* lb, const uint32_t* fid, int valid,
-                                               bool stage_lb, uint32_t my_f, int lane) {
+                                               bool stage_lb, uint32_t my_f, int lane, float* sdk) {
     const float K = 1.000001f;
     const float delta = p.f32_delta;
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
     uint32_t mask = 0;
+    if (active && sdk) {                         // the row's bound as tightened by the other replicas
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        const float v = *sdk;
+        if (v < dkx) DK = pk2(v, v);
+    }
     if (active) {
 #pragma unroll
         for (int pp = 0; pp < 16; ++pp) {
@@ -306,7 +312,12 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
             // any upper bound of sqrt(best) is a valid d_min for the prunes: the fp32 sqrt rounded up of
             // best rounded up (cheaper than the fp64 sqrt)
             const float dkf = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(dd)), delta), K);
-            DK = pk2(dkf, dkf);
+            float dkx, dky;
+            upk2(DK, dkx, dky);
+            if (dkf < dkx) {
+                DK = pk2(dkf, dkf);
+                if (sdk) atomicMin(reinterpret_cast<int*>(sdk), __float_as_int(dkf));  // >= 0: int order
+            }
         }
         return true;
     };
@@ -504,7 +515,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
             __syncwarp();
             if (kCounters && lane == 0) sbytes += 20ull * valid;  // staged ids + fp32 records
             scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      wp, wl, wf, valid, true, f, lane);
+                                      wp, wl, wf, valid, true, f, lane, nullptr);
             __syncwarp();                        // the slice is rewritten by the next batch
         }
     }
@@ -580,6 +591,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     __shared__ double s_rd[kTile];
     __shared__ uint32_t s_rf[kTile];
     __shared__ uint32_t s_re[kTile];
+    __shared__ float s_dk[kTile];                // per row: the tightest d_min bound any replica found
     const uint32_t nt = meta[0];
     if (blockIdx.x >= nt - meta[2]) return;     // invalid, or a small tile (k_scan_small)
     const uint32_t b = order[blockIdx.x];        // launch order: site order or longest-first
@@ -642,6 +654,19 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     }
 #endif
     if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK);
+    if (active && r == 0) {                      // replicas share one pruning bound per row
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        s_dk[j] = dkx;
+    }
+    auto refresh_dk = [&]() {                    // the row's bound as tightened by the other replicas
+        if (R > 1 && active) {
+            float dkx, dky;
+            upk2(DK, dkx, dky);
+            const float v = s_dk[j];
+            if (v < dkx) DK = pk2(v, v);
+        }
+    };
 #if P2M_EARLY1 >= 2
     if (early && tid < (int)min((uint64_t)kChunk, end - beg)) {
         // the chunk's lower-bound records, async into shared memory (nf has landed by now); waited
@@ -740,7 +765,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
                               uint32_t my_f) {
             scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      pair, lb, fid, valid, stage_lb, my_f, lane);
+                                      pair, lb, fid, valid, stage_lb, my_f, lane, R > 1 && active ? &s_dk[j] : nullptr);
         };
         if (G == 1) {
             // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
@@ -765,6 +790,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 if (b0 >= end) continue;
                 const int valid = (int)min((uint64_t)32, end - b0);
                 bool need = p.no_batch != 0;
+                refresh_dk();
                 if (active && !need) {
                     const float4 c = p.bsph[bo + gb];
                     float dkx, dky;
@@ -825,6 +851,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             if (tid == 0) s_need = 0u;
             __syncthreads();
             uint32_t wneed = 0;
+            refresh_dk();
             if (warp_on) {
                 for (int bb = r; bb < nb; bb += R) {
                     bool need = p.no_batch != 0;

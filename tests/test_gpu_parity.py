@@ -488,3 +488,46 @@ def test_device_image_round_trip(c2, tmp_path):
     two = P.Engine.load(path, devices=[0, 0])
     r2 = two.batch_query(q)
     assert r2.distance.tobytes() == r0.distance.tobytes() and np.array_equal(r2.face, r0.face)
+
+
+def test_device_built_grid_without_cell_boxes(c2):
+    """An external builder's desc without Voronoi cell boxes (site_cell_box = NULL): the engine
+    builds the exact cell-locate grid on the device from the sites alone (p2m_grid.cu) instead of
+    falling back to the per-thread k-d descent.  Rows are bit-identical to the box-built grid and to
+    the oracle; the descent time is reported against the box-built grid."""
+    import torch
+    V, F, h = c2
+    d = h.desc()
+    d.site_cell_box = None
+    eng_dev = P.Engine.from_desc(d)
+    eng_box = P.Engine(h)
+    q = P.gen_queries(2, V, F, 0, 2_000_000)
+    a, b = eng_dev.batch_query(q), eng_box.batch_query(q)
+    for k in ("distance", "closest", "face", "site", "flags"):
+        assert getattr(a, k).tobytes() == getattr(b, k).tobytes(), k
+    ref = oracle_checker(h.arrays()).batch_query(q[:300_000], prune=O.PRUNE_SAFE)
+    for k in ("site", "face"):
+        assert np.array_equal(getattr(a, k)[:300_000], ref[k]), k
+    assert a.distance[:300_000].tobytes() == ref["distance"].tobytes()
+    # grid candidates per query (kd_nodes_visited counts them): same order of magnitude
+    assert a.counters["kd_nodes_visited"] <= 4 * b.counters["kd_nodes_visited"]
+    n = len(q)
+    dq = torch.from_numpy(q).cuda()
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty((n, 3), dtype=torch.float64, device="cuda")] + \
+           [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]
+    vp = lambda t: C.c_void_p(t.data_ptr())
+    lib = L.cuda()
+    t = {}
+    for name, e in (("device_grid", eng_dev), ("box_grid", eng_box)):
+        for _ in range(2):
+            L.check(lib.p2m_query_device(e.handle, 0, vp(dq), n, *[vp(x) for x in outs], None, None))
+        L.check(lib.p2m_set_profiling(e.handle, 1))
+        for _ in range(5):
+            L.check(lib.p2m_query_device(e.handle, 0, vp(dq), n, *[vp(x) for x in outs], None, None))
+        torch.cuda.synchronize()
+        ms = (C.c_float * 6)()
+        L.check(lib.p2m_last_timings(e.handle, 0, ms))
+        L.check(lib.p2m_set_profiling(e.handle, 0))
+        t[name] = ms[2]
+    print(f"descent ms: device-built grid {t['device_grid']:.3f}, box grid {t['box_grid']:.3f}")
+    assert t["device_grid"] <= 3.0 * t["box_grid"]
