@@ -79,7 +79,7 @@ __device__ __forceinline__ void load_tri(const D4* rec, V* a, V* b, V* c) {
     *c = V{t1.z, t1.w, t2.x};
 }
 
-constexpr int kLbRec = 6;   // float4 per fp32 lower-bound record (p2m_grouped.cu lb2_face)
+constexpr int kCy = 2;      // float4 per bounding-cylinder record (Params::fcy / bcy / ccy)
 constexpr uint64_t kIdMask = 0xffffffffull;
 constexpr int kDimShift = 32;
 constexpr uint64_t kSentinelBit = 1ull << 34;
@@ -88,17 +88,18 @@ struct Params {
     const D4* kd;           // S nodes
     uint32_t n_nodes;
     const D4* rec;          // 4 per face
-    const float4* f32;      // per face fp32 pre-filter record: c rounded to nearest, r_up * K rounded up
-    const float4* lbr;      // per face kLbRec = 6 x float4: a, unit normal n, in-plane outward edge normals
-                            // m_ab, m_bc, m_ca, offset m_bc.(b-a), b, c -- the tight lower bound (lb2_face)
-    float lb_margin;        // absolute fp32 error bound of that lower bound (64 * 2^-24 * M)
+    // bounding cylinders (kCy = 2 float4 each: {c.xyz, 4 R^2}, {n.xyz, t}; every point x of every member
+    // face has |nn.(x - c)| <= t and in-plane distance <= R, nn = n / |n|; p2m_engine.cu fit_cyl):
+    const float4* fcy;      // per face (its bounding disk: level 2 of the grouped scan)
+    const float4* bcy;      // per aligned 32-entry batch of lfs (level 1)
+    const float4* ccy;      // per aligned 256-entry chunk of lfs (level 0)
     const uint64_t* off;    // S+1
     const uint64_t* boff;   // S+1: first batch sphere of each list (one per aligned 32 entries of lfs)
-    const float4* bsph;     // batch spheres: centre rounded to nearest, radius (rounded up) * K
+    const float4* bpt;      // per batch: {a point ON the mesh near the batch centre (fp32), 0} -- d_min seeds
     const uint32_t* lf;     // list entries, ascending (REF/SPEC.md:392; the fused sequential path)
     const uint32_t* lfs;    // the same lists in spatial (Morton) order (the grouped scan)
     const uint64_t* coff;   // S+1: first chunk sphere of each list (one per aligned 256 entries of lfs)
-    const float4* csph;     // chunk spheres, same conservative form as bsph
+    const float4* cpt;      // per chunk: the same for the chunk
     const D4* bvh;          // 2 per node
     const uint32_t* bvh_perm;  // leaf face ids
     uint32_t n_faces;

@@ -27,6 +27,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "../../../include/p2m.h"
+#include "../host/geom.hpp"
 #include "p2m_device.cuh"
 #include "p2m_kernels.cuh"
 
@@ -36,7 +37,7 @@ extern "C" void p2m_set_last_error_internal(const char* msg);  // libp2m_host.so
 
 using p2m::dev::D4;
 using p2m::dev::Params;
-using p2m::dev::kLbRec;
+using p2m::dev::kCy;
 
 namespace {
 
@@ -71,6 +72,64 @@ void parallel_sites(uint64_t S, Fn&& fn) {
             }
         });
     for (auto& x : th) x.join();
+}
+
+float round_up_f(double v) {
+    float f = (float)v;
+    if ((double)f < v) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+// Bounding cylinder of a set of faces for the scan's fp32 lower bound (p2m_grouped.cu cyl_near /
+// the disk test): x = the faces' vertices (a face is the convex hull of its vertices and the cylinder
+// is convex).  Axis n = the fp32 rounding of the unit area-weighted normal sum, centre c in fp32
+// (cen if given -- a face's min-enclosing-sphere centre -- else the middle of the points' extents along
+// n and two in-plane directions).  With nn = n / |n| in exact arithmetic, every point satisfies
+// |nn.(x - c)| <= t and |x - c|^2 - (nn.(x - c))^2 <= R^2.  Stored {c, 4 R^2} and {n, t + tslack},
+// both rounded up and inflated by 1e-12 (relative, and of the points' extent from c) over the fp64
+// evaluation here; tslack = the device's fp32 error of |h|.
+void fit_cyl(const double* x, int m, const double* nsum, const double* cen, double tslack, float4* out) {
+    double n[3] = {nsum[0], nsum[1], nsum[2]};
+    double l = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    if (!(l > 0.0) || !std::isfinite(l)) { n[0] = 0.0; n[1] = 0.0; n[2] = 1.0; l = 1.0; }
+    const float nf[3] = {(float)(n[0] / l), (float)(n[1] / l), (float)(n[2] / l)};
+    const double lf = std::sqrt((double)nf[0] * nf[0] + (double)nf[1] * nf[1] + (double)nf[2] * nf[2]);
+    const double nn[3] = {nf[0] / lf, nf[1] / lf, nf[2] / lf};
+    double C[3];
+    if (cen) {
+        for (int k = 0; k < 3; ++k) C[k] = cen[k];
+    } else {
+        // in-plane basis e1, e2 perpendicular to nn
+        double a[3] = {0.0, 0.0, 0.0};
+        a[std::fabs(nn[0]) < 0.6 ? 0 : (std::fabs(nn[1]) < 0.6 ? 1 : 2)] = 1.0;
+        double e1[3] = {a[1] * nn[2] - a[2] * nn[1], a[2] * nn[0] - a[0] * nn[2], a[0] * nn[1] - a[1] * nn[0]};
+        const double l1 = std::sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+        for (double& v : e1) v /= l1;
+        const double e2[3] = {nn[1] * e1[2] - nn[2] * e1[1], nn[2] * e1[0] - nn[0] * e1[2], nn[0] * e1[1] - nn[1] * e1[0]};
+        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int i = 0; i < m; ++i) {
+            const double* p = x + 3 * i;
+            const double c3[3] = {nn[0] * p[0] + nn[1] * p[1] + nn[2] * p[2], e1[0] * p[0] + e1[1] * p[1] + e1[2] * p[2],
+                                  e2[0] * p[0] + e2[1] * p[1] + e2[2] * p[2]};
+            for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], c3[k]); hi[k] = std::max(hi[k], c3[k]); }
+        }
+        const double mh = 0.5 * (lo[0] + hi[0]), m1 = 0.5 * (lo[1] + hi[1]), m2 = 0.5 * (lo[2] + hi[2]);
+        for (int k = 0; k < 3; ++k) C[k] = nn[k] * mh + e1[k] * m1 + e2[k] * m2;
+    }
+    const float cf[3] = {(float)C[0], (float)C[1], (float)C[2]};
+    double t = 0.0, r2 = 0.0, d2m = 0.0;
+    for (int i = 0; i < m; ++i) {
+        const double v[3] = {x[3 * i] - cf[0], x[3 * i + 1] - cf[1], x[3 * i + 2] - cf[2]};
+        const double h = nn[0] * v[0] + nn[1] * v[1] + nn[2] * v[2];
+        const double d2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+        t = std::max(t, std::fabs(h));
+        r2 = std::max(r2, d2 - h * h);
+        d2m = std::max(d2m, d2);
+    }
+    t = t * (1.0 + 1e-12) + 1e-12 * std::sqrt(d2m) + tslack;
+    r2 = r2 * (1.0 + 1e-12) + 1e-12 * d2m;
+    out[0] = make_float4(cf[0], cf[1], cf[2], round_up_f(4.0 * r2));
+    out[1] = make_float4(nf[0], nf[1], nf[2], round_up_f(t));
 }
 
 uint64_t lb_left_size(uint64_t n) {
@@ -251,10 +310,11 @@ struct Slot {
     int dev = 0;
     cudaStream_t stream = nullptr;
     D4 *kd = nullptr, *rec = nullptr, *bvh = nullptr;
-    float4* f32 = nullptr;
-    float4* bsph = nullptr;
-    float4* csph = nullptr;
-    float4* lbr = nullptr;
+    float4* fcy = nullptr;   // kCy float4 per face / batch / chunk: the bounding cylinders
+    float4* bcy = nullptr;
+    float4* ccy = nullptr;
+    float4* bpt = nullptr;
+    float4* cpt = nullptr;
     uint64_t* boff = nullptr;
     uint64_t* coff = nullptr;
     uint64_t* off = nullptr;
@@ -338,9 +398,9 @@ void free_slot(Slot& s) {
     cudaFree(s.kd); cudaFree(s.rec); cudaFree(s.bvh); cudaFree(s.off); cudaFree(s.lf); cudaFree(s.bvh_perm);
     cudaFree(s.heavy);
     cudaFree(s.site_pos); cudaFree(s.site_ref); cudaFree(s.grid_off); cudaFree(s.grid_site);
-    cudaFree(s.f32);
-    cudaFree(s.bsph); cudaFree(s.boff); cudaFree(s.lbr);
-    cudaFree(s.csph); cudaFree(s.coff); cudaFree(s.lfs);
+    cudaFree(s.fcy); cudaFree(s.bcy); cudaFree(s.ccy);
+    cudaFree(s.bpt); cudaFree(s.boff);
+    cudaFree(s.cpt); cudaFree(s.coff); cudaFree(s.lfs);
     cudaFree(s.adj_off); cudaFree(s.adj);
     for (auto& w : s.ws) {
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
@@ -496,14 +556,15 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
     CK(cudaEventCreateWithFlags(&s.agg_ready, cudaEventDisableTiming));
     CK(cudaMalloc(&s.kd, sizeof(D4) * std::max<uint64_t>(1, E.n_sites)));
     CK(cudaMalloc(&s.rec, sizeof(D4) * 4 * std::max<uint64_t>(1, E.n_faces)));
-    CK(cudaMalloc(&s.f32, sizeof(float4) * std::max<uint64_t>(1, E.n_faces)));
-    CK(cudaMalloc(&s.bsph, sizeof(float4) * std::max<uint64_t>(1, E.n_batches)));
-    CK(cudaMalloc(&s.lbr, sizeof(float4) * kLbRec * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.fcy, sizeof(float4) * kCy * std::max<uint64_t>(1, E.n_faces)));
+    CK(cudaMalloc(&s.bcy, sizeof(float4) * kCy * std::max<uint64_t>(1, E.n_batches)));
+    CK(cudaMalloc(&s.ccy, sizeof(float4) * kCy * std::max<uint64_t>(1, E.n_chunks)));
+    CK(cudaMalloc(&s.bpt, sizeof(float4) * std::max<uint64_t>(1, E.n_batches)));
     CK(cudaMalloc(&s.boff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.off, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.lf, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
     CK(cudaMalloc(&s.lfs, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_entries)));
-    CK(cudaMalloc(&s.csph, sizeof(float4) * std::max<uint64_t>(1, E.n_chunks)));
+    CK(cudaMalloc(&s.cpt, sizeof(float4) * std::max<uint64_t>(1, E.n_chunks)));
     CK(cudaMalloc(&s.coff, sizeof(uint64_t) * (E.n_sites + 1)));
     CK(cudaMalloc(&s.bvh, sizeof(D4) * 2 * std::max<uint64_t>(1, E.n_bvh)));
     CK(cudaMalloc(&s.bvh_perm, sizeof(uint32_t) * std::max<uint64_t>(1, E.n_faces)));
@@ -760,7 +821,7 @@ struct Image {
         uint64_t bytes() const { return sizeof(T) * n; }
     };
     Arr<D4> kd, rec, bvh, site_pos, site_ref;
-    Arr<float4> f32, bsph, csph, lbr;
+    Arr<float4> fcy, bcy, ccy, bpt, cpt;
     Arr<uint64_t> boff, coff, off, adj_off;
     Arr<uint32_t> lf, lfs, bvh_perm, grid_off, grid_site, adj;
     Arr<uint8_t> heavy;   // empty: estimate at creation (mark_heavy_sites)
@@ -784,10 +845,11 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
     struct Up { void* dst; const void* src; size_t n; };
     auto uploads = [&](Slot& s) {
         return std::vector<Up>{
-            {s.kd, I.kd.p, I.kd.bytes()}, {s.rec, I.rec.p, I.rec.bytes()}, {s.f32, I.f32.p, I.f32.bytes()},
-            {s.bsph, I.bsph.p, I.bsph.bytes()}, {s.boff, I.boff.p, I.boff.bytes()}, {s.lbr, I.lbr.p, I.lbr.bytes()},
+            {s.kd, I.kd.p, I.kd.bytes()}, {s.rec, I.rec.p, I.rec.bytes()}, {s.fcy, I.fcy.p, I.fcy.bytes()},
+            {s.bcy, I.bcy.p, I.bcy.bytes()}, {s.ccy, I.ccy.p, I.ccy.bytes()},
+            {s.bpt, I.bpt.p, I.bpt.bytes()}, {s.boff, I.boff.p, I.boff.bytes()},
             {s.off, I.off.p, I.off.bytes()}, {s.lf, I.lf.p, I.lf.bytes()}, {s.lfs, I.lfs.p, I.lfs.bytes()},
-            {s.csph, I.csph.p, I.csph.bytes()}, {s.coff, I.coff.p, I.coff.bytes()}, {s.bvh, I.bvh.p, I.bvh.bytes()},
+            {s.cpt, I.cpt.p, I.cpt.bytes()}, {s.coff, I.coff.p, I.coff.bytes()}, {s.bvh, I.bvh.p, I.bvh.bytes()},
             {s.bvh_perm, I.bvh_perm.p, I.bvh_perm.bytes()}, {s.site_pos, I.site_pos.p, I.site_pos.bytes()},
             {s.site_ref, I.site_ref.p, I.site_ref.bytes()},
             {s.adj_off, I.adj_off.p, E->has_adj ? I.adj_off.bytes() : 0}, {s.adj, I.adj.p, E->has_adj ? I.adj.bytes() : 0},
@@ -832,8 +894,8 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
     E->replicate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto& s : E->slots) {
         s->params = P;
-        s->params.kd = s->kd; s->params.rec = s->rec; s->params.f32 = s->f32; s->params.bsph = s->bsph; s->params.boff = s->boff; s->params.lbr = s->lbr; s->params.off = s->off; s->params.lf = s->lf;
-        s->params.lfs = s->lfs; s->params.csph = s->csph; s->params.coff = s->coff;
+        s->params.kd = s->kd; s->params.rec = s->rec; s->params.fcy = s->fcy; s->params.bcy = s->bcy; s->params.ccy = s->ccy; s->params.bpt = s->bpt; s->params.boff = s->boff; s->params.off = s->off; s->params.lf = s->lf;
+        s->params.lfs = s->lfs; s->params.cpt = s->cpt; s->params.coff = s->coff;
         s->params.bvh = s->bvh; s->params.bvh_perm = s->bvh_perm; s->params.heavy = s->heavy;
         s->params.site_pos = s->site_pos;
         s->params.site_ref = s->site_ref;
@@ -930,18 +992,33 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         std::memcpy(&p1, fn + 2, 8);
         rec[4 * f + 3] = D4{t[8], p0, p1, 0.0};
     }
-    // fp32 pre-filter records (k_scan_tiles): centre rounded to nearest, radius rounded up and
-    // multiplied by K = 1.000001 rounding up -- the same values the kernel's bound assumes
-    std::vector<float4> f32(F);
-    for (uint64_t f = 0; f < F; ++f) {
-        const double* sp = d->face_sphere + 4 * f;
-        float r = (float)sp[3];
-        if ((double)r < sp[3]) r = std::nextafter(r, INFINITY);
-        const double prod = (double)r * (double)1.000001f;
-        float rk = (float)prod;
-        if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
-        f32[f] = make_float4((float)sp[0], (float)sp[1], (float)sp[2], rk);
-    }
+    // fp32 bound of the scan's level 2: each face's bounding disk (a cylinder of height ~0 around its
+    // min-enclosing-sphere centre), DESIGN.md section 9.  M = max |coordinate| of D scales the
+    // device's fp32 error terms.
+    double Mdom = 0.0;
+    for (int c = 0; c < 3; ++c) Mdom = std::max({Mdom, std::fabs(d->domain_min[c]), std::fabs(d->domain_max[c])});
+    const double tslack = 40.0 * std::ldexp(1.0, -24) * Mdom;
+    std::vector<float4> fcy(kCy * F);
+    auto group_normal = [&](const uint32_t* ids, uint64_t k, double* nsum, std::vector<double>& pts) {
+        nsum[0] = nsum[1] = nsum[2] = 0.0;
+        pts.resize(9 * k);
+        for (uint64_t i = 0; i < k; ++i) {
+            const double* t = d->tri_xyz + 9 * (uint64_t)(ids ? ids[i] : i);
+            for (int c = 0; c < 9; ++c) pts[9 * i + c] = t[c];
+            const double ux = t[3] - t[0], uy = t[4] - t[1], uz = t[5] - t[2];
+            const double vx = t[6] - t[0], vy = t[7] - t[1], vz = t[8] - t[2];
+            nsum[0] += uy * vz - uz * vy; nsum[1] += uz * vx - ux * vz; nsum[2] += ux * vy - uy * vx;
+        }
+    };
+    parallel_sites(F, [&](uint64_t f0, uint64_t f1) {
+        std::vector<double> pts;
+        double ns[3];
+        for (uint64_t f = f0; f < f1; ++f) {
+            const uint32_t id = (uint32_t)f;
+            group_normal(&id, 1, ns, pts);
+            fit_cyl(pts.data(), 3, ns, d->face_sphere + 4 * f, tslack, fcy.data() + kCy * f);
+        }
+    });
     // Spatial list order for the grouped scan (lfs): the (d^2, face id) argmin does not depend on
     // the order a list is scanned in, so each list is re-sorted by the Morton code of its faces'
     // sphere centres (ties by id) -- its 32-entry batches and 256-entry chunks then enclose compact
@@ -986,33 +1063,25 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             }
         });
     }
-    // level-1 / level-0 pruning spheres over lfs: one per aligned 32-entry batch and one per aligned
-    // 256-entry chunk of every list.  Centre = centre of the members' sphere boxes; radius =
-    // max |c_i - C| + r_i, then made conservative for the fp32 kernel test (centre rounded to
-    // nearest, radius grown by the centre's rounding and rounded up, times K rounded up -- the same
-    // form as the per-face records)
-    auto group_sphere = [&](uint64_t j, uint64_t je) {
+    // d_min seed points over lfs, one per aligned 32-entry batch and one per aligned 256-entry chunk:
+    // a point ON the mesh near the group's centre (the closest point of the member faces to the centre
+    // of their sphere boxes), rounded to fp32 -- |q - P| + the rounding slack bounds d(q, M) from above
+    auto group_point = [&](uint64_t j, uint64_t je) {
         double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         for (uint64_t t = j; t < je; ++t) {
             const double* sp = d->face_sphere + 4 * (uint64_t)lfs[t];
             for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], sp[k] - sp[3]); hi[k] = std::max(hi[k], sp[k] + sp[3]); }
         }
-        double C[3] = {0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
-        float cf[3] = {(float)C[0], (float)C[1], (float)C[2]};
-        double R = 0.0;
+        const p2m::V3 C{0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+        double bd = INFINITY;
+        p2m::V3 P{0, 0, 0};
         for (uint64_t t = j; t < je; ++t) {
-            const double* sp = d->face_sphere + 4 * (uint64_t)lfs[t];
-            double dd = 0.0;
-            for (int k = 0; k < 3; ++k) dd += (sp[k] - (double)cf[k]) * (sp[k] - (double)cf[k]);
-            R = std::max(R, std::sqrt(dd) + sp[3]);
+            const double* tr = d->tri_xyz + 9 * (uint64_t)lfs[t];
+            p2m::V3 cp;
+            const double dd = p2m::closest_tri(C, p2m::ld3(tr), p2m::ld3(tr + 3), p2m::ld3(tr + 6), &cp);
+            if (dd < bd) { bd = dd; P = cp; }
         }
-        R = R * (1.0 + 1e-12) + 1e-300;
-        float rf = (float)R;
-        if ((double)rf < R) rf = std::nextafter(rf, INFINITY);
-        const double prod = (double)rf * (double)1.000001f;
-        float rk = (float)prod;
-        if ((double)rk < prod) rk = std::nextafter(rk, INFINITY);
-        return make_float4(cf[0], cf[1], cf[2], rk);
+        return make_float4((float)P.x, (float)P.y, (float)P.z, 0.0f);
     };
     std::vector<uint64_t> boff(S + 1, 0), coff(S + 1, 0);
     for (uint64_t s = 0; s < S; ++s) {
@@ -1022,48 +1091,27 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     }
     E->n_batches = boff[S];
     E->n_chunks = coff[S];
-    std::vector<float4> bsph(std::max<uint64_t>(1, E->n_batches)), csph(std::max<uint64_t>(1, E->n_chunks));
+    std::vector<float4> bpt(std::max<uint64_t>(1, E->n_batches)), cpt(std::max<uint64_t>(1, E->n_chunks));
+    std::vector<float4> bcy(kCy * std::max<uint64_t>(1, E->n_batches)), ccy(kCy * std::max<uint64_t>(1, E->n_chunks));
     parallel_sites(S, [&](uint64_t s0, uint64_t s1) {
+        std::vector<double> pts;
+        double ns[3];
         for (uint64_t s = s0; s < s1; ++s) {
             const uint64_t b0 = d->list_offsets[s], b1 = d->list_offsets[s + 1];
-            for (uint64_t j = b0, bi = boff[s]; j < b1; j += 32, ++bi) bsph[bi] = group_sphere(j, std::min(b1, j + 32));
-            for (uint64_t j = b0, ci = coff[s]; j < b1; j += kListChunk, ++ci)
-                csph[ci] = group_sphere(j, std::min(b1, j + kListChunk));
+            for (uint64_t j = b0, bi = boff[s]; j < b1; j += 32, ++bi) {
+                const uint64_t je = std::min(b1, j + 32);
+                bpt[bi] = group_point(j, je);
+                group_normal(lfs.data() + j, je - j, ns, pts);
+                fit_cyl(pts.data(), (int)(3 * (je - j)), ns, nullptr, tslack, bcy.data() + kCy * bi);
+            }
+            for (uint64_t j = b0, ci = coff[s]; j < b1; j += kListChunk, ++ci) {
+                const uint64_t je = std::min(b1, j + kListChunk);
+                cpt[ci] = group_point(j, je);
+                group_normal(lfs.data() + j, je - j, ns, pts);
+                fit_cyl(pts.data(), (int)(3 * (je - j)), ns, nullptr, tslack, ccy.data() + kCy * ci);
+            }
         }
     });
-    // tight fp32 lower-bound records (the scan's rare path, p2m_grouped.cu lb2_face): d(q,T)^2 >=
-    // h^2 + max(0, s_i)^2 with h = n.(q-a) and s_i the signed in-plane distances to the three edge
-    // lines (outward positive), and the support bound along q - V for the nearest vertex V (b, c)
-    std::vector<float4> lbr(kLbRec * std::max<uint64_t>(1, F));
-    for (uint64_t f = 0; f < F; ++f) {
-        const double* t = d->tri_xyz + 9 * f;
-        const double A[3] = {t[0], t[1], t[2]}, B[3] = {t[3], t[4], t[5]}, Cc[3] = {t[6], t[7], t[8]};
-        auto sub3 = [](const double* x, const double* y, double* o) { for (int k = 0; k < 3; ++k) o[k] = x[k] - y[k]; };
-        auto crs = [](const double* x, const double* y, double* o) {
-            o[0] = x[1] * y[2] - x[2] * y[1]; o[1] = x[2] * y[0] - x[0] * y[2]; o[2] = x[0] * y[1] - x[1] * y[0];
-        };
-        auto unit = [](double* v) {
-            const double l = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-            if (l > 0.0 && std::isfinite(l)) { v[0] /= l; v[1] /= l; v[2] /= l; return true; }
-            v[0] = v[1] = v[2] = 0.0;
-            return false;
-        };
-        double ab[3], ac[3], bc[3], ca[3], n[3], m1[3], m2[3], m3[3];
-        sub3(B, A, ab); sub3(Cc, A, ac); sub3(Cc, B, bc); sub3(A, Cc, ca);
-        crs(ab, ac, n);
-        bool ok = unit(n);
-        crs(ab, n, m1); crs(bc, n, m2); crs(ca, n, m3);
-        ok = ok && unit(m1) && unit(m2) && unit(m3);
-        if (!ok) { for (int k = 0; k < 3; ++k) n[k] = m1[k] = m2[k] = m3[k] = 0.0; }  // never prunes
-        const double o2 = ok ? (m2[0] * ab[0] + m2[1] * ab[1] + m2[2] * ab[2]) : 0.0;
-        float4* L = lbr.data() + kLbRec * f;
-        L[0] = make_float4((float)A[0], (float)A[1], (float)A[2], (float)n[0]);
-        L[1] = make_float4((float)n[1], (float)n[2], (float)m1[0], (float)m1[1]);
-        L[2] = make_float4((float)m1[2], (float)m2[0], (float)m2[1], (float)m2[2]);
-        L[3] = make_float4((float)m3[0], (float)m3[1], (float)m3[2], (float)o2);
-        L[4] = make_float4((float)B[0], (float)B[1], (float)B[2], (float)Cc[0]);
-        L[5] = make_float4((float)Cc[1], (float)Cc[2], 0.f, 0.f);
-    }
     FlatBvh bvh;
     build_bvh(d->tri_xyz, F, bvh);
     E->n_bvh = bvh.nodes.size() / 2;
@@ -1087,12 +1135,6 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         float df = (float)delta;
         if ((double)df < delta) df = std::nextafter(df, INFINITY);
         P.f32_delta = df;
-        // lower-bound record error: each dot product of a unit vector with fl(q_f - a_f) is within
-        // ~25*2^-24*M of exact, the edge offset adds ~4*2^-24*M; 64*2^-24*M covers both with margin
-        const double lm = 64.0 * std::ldexp(1.0, -24) * M;
-        float lmf = (float)lm;
-        if ((double)lmf < lm) lmf = std::nextafter(lmf, INFINITY);
-        P.lb_margin = lmf;
     }
     P.long_tile = 32;
     if (const char* v = std::getenv("P2M_LONG_TILE")) {
@@ -1139,10 +1181,11 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     }
     // ---- upload to the first device, peer-replicate to the rest ----
     Image I;
-    I.kd.set(kd.data(), S); I.rec.set(rec.data(), 4 * F); I.f32.set(f32.data(), F);
-    I.bsph.set(bsph.data(), bsph.size()); I.boff.set(boff.data(), S + 1); I.lbr.set(lbr.data(), lbr.size());
+    I.kd.set(kd.data(), S); I.rec.set(rec.data(), 4 * F); I.fcy.set(fcy.data(), fcy.size());
+    I.bpt.set(bpt.data(), bpt.size()); I.boff.set(boff.data(), S + 1);
+    I.bcy.set(bcy.data(), bcy.size()); I.ccy.set(ccy.data(), ccy.size());
     I.off.set(d->list_offsets, S + 1); I.lf.set(d->list_faces, L); I.lfs.set(lfs.data(), L);
-    I.csph.set(csph.data(), csph.size()); I.coff.set(coff.data(), S + 1);
+    I.cpt.set(cpt.data(), cpt.size()); I.coff.set(coff.data(), S + 1);
     I.bvh.set(bvh.nodes.data(), bvh.nodes.size()); I.bvh_perm.set(bvh.perm.data(), F);
     I.site_pos.set(site_pos.data(), S); I.site_ref.set(site_ref.data(), S);
     if (E->has_adj) { I.adj_off.set(d->adj_offsets, S + 1); I.adj.set(d->adj_sites, E->n_adj); }
@@ -1166,7 +1209,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
 // monotonicity and every stored id against its range before anything reaches a device.
 namespace {
 
-constexpr uint32_t kImageVersion = 1;
+constexpr uint32_t kImageVersion = 2;  // v2: bounding cylinders (fcy/bcy/ccy) replace the v1 sphere/plane records
 
 struct Fnv {
     uint64_t h = 1469598103934665603ull;
@@ -1204,7 +1247,7 @@ struct Reader {
 template <class IO, class F>
 void params_fields(Params& P, F&& f) {
     for (int c = 0; c < 3; ++c) { f(P.dmin[c]); f(P.dmax[c]); f(P.key_lo[c]); f(P.key_scale[c]); f(P.grid_lo[c]); f(P.grid_inv[c]); f(P.grid_res[c]); }
-    f(P.prune_eps); f(P.f32_delta); f(P.lb_margin); f(P.long_tile); f(P.no_seed); f(P.no_batch); f(P.n_nodes); f(P.n_faces);
+    f(P.prune_eps); f(P.f32_delta); f(P.long_tile); f(P.no_seed); f(P.no_batch); f(P.n_nodes); f(P.n_faces);
 }
 
 template <class T>
@@ -1230,8 +1273,8 @@ P2M_API int p2m_engine_save(const p2m_engine* e, const char* path) {
     CK(cudaDeviceSynchronize());
     struct A { const void* dev; uint64_t bytes; };
     const A arrs[] = {
-        {s.kd, 32 * S}, {s.rec, 128 * F}, {s.f32, 16 * F}, {s.bsph, 16 * e->n_batches}, {s.boff, 8 * (S + 1)},
-        {s.lbr, 16ull * kLbRec * F}, {s.off, 8 * (S + 1)}, {s.lf, 4 * L}, {s.lfs, 4 * L}, {s.csph, 16 * e->n_chunks},
+        {s.kd, 32 * S}, {s.rec, 128 * F}, {s.fcy, 16ull * kCy * F}, {s.bcy, 16ull * kCy * e->n_batches},
+        {s.ccy, 16ull * kCy * e->n_chunks}, {s.bpt, 16 * e->n_batches}, {s.boff, 8 * (S + 1)}, {s.off, 8 * (S + 1)}, {s.lf, 4 * L}, {s.lfs, 4 * L}, {s.cpt, 16 * e->n_chunks},
         {s.coff, 8 * (S + 1)}, {s.bvh, 64 * e->n_bvh}, {s.bvh_perm, 4 * F}, {s.site_pos, 32 * S}, {s.site_ref, 32 * S},
         {s.adj_off, e->has_adj ? 8 * (S + 1) : 0}, {s.adj, e->has_adj ? 4 * e->n_adj : 0},
         {s.grid_off, e->grid_cells ? 4 * (e->grid_cells + 1) : 0}, {s.grid_site, e->grid_cells ? 4 * e->grid_pairs : 0},
@@ -1307,8 +1350,8 @@ P2M_API int p2m_engine_load(const char* path, int n_devices, const int* device_i
         r.get(v.data(), bytes);
         arr.take(std::move(v));
     };
-    rd(I.kd, S); rd(I.rec, 4 * F); rd(I.f32, F); rd(I.bsph, E->n_batches); rd(I.boff, S + 1);
-    rd(I.lbr, (uint64_t)kLbRec * F); rd(I.off, S + 1); rd(I.lf, L); rd(I.lfs, L); rd(I.csph, E->n_chunks);
+    rd(I.kd, S); rd(I.rec, 4 * F); rd(I.fcy, (uint64_t)kCy * F); rd(I.bcy, (uint64_t)kCy * E->n_batches);
+    rd(I.ccy, (uint64_t)kCy * E->n_chunks); rd(I.bpt, E->n_batches); rd(I.boff, S + 1); rd(I.off, S + 1); rd(I.lf, L); rd(I.lfs, L); rd(I.cpt, E->n_chunks);
     rd(I.coff, S + 1); rd(I.bvh, 2 * E->n_bvh); rd(I.bvh_perm, F); rd(I.site_pos, S); rd(I.site_ref, S);
     rd(I.adj_off, E->has_adj ? S + 1 : 0); rd(I.adj, E->has_adj ? E->n_adj : 0);
     rd(I.grid_off, E->grid_cells ? E->grid_cells + 1 : 0); rd(I.grid_site, E->grid_cells ? E->grid_pairs : 0);

@@ -174,74 +174,106 @@ __device__ __forceinline__ uint64_t mul2_up(uint64_t a, uint64_t b) {
     return r;
 }
 
-// Tight lower bound of d(q, T)^2 from a staged 96-byte record (a, n, m_ab, m_bc, m_ca, o_bc, b, c):
-// the max of two valid bounds, each exact in its own Voronoi region of the triangle --
-//  * h^2 + max(0, s_ab, s_bc, s_ca)^2, h = n.(q-a), s_i the signed in-plane edge-line distances (the
-//    triangle is the intersection of three half-planes): exact when the closest point is interior
-//    or on an edge;
-//  * the support-function bound along m = q - V for the vertex V nearest to q: d(q, T) >=
-//    min_i m.(q - v_i) / |m| for ANY vector m (T lies in the half-space {x : m.x <= max_i m.v_i}),
-//    which equals |q - V| when the closest point is the vertex V.
-// (Measured on c2: faces whose bound is <= the final distance drop from 32 to 3 per row.)  fp32
-// error <= Params::lb_margin.
-__device__ __forceinline__ float lb2_plane(const float4* r, float qx, float qy, float qz) {
-    const float4 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3];
-    const float dx = qx - r0.x, dy = qy - r0.y, dz = qz - r0.z;
-    const float hh = __fmaf_rn(r0.w, dx, __fmaf_rn(r1.x, dy, __fmul_rn(r1.y, dz)));
-    const float s1 = __fmaf_rn(r1.z, dx, __fmaf_rn(r1.w, dy, __fmul_rn(r2.x, dz)));
-    const float s2 = __fmaf_rn(r2.y, dx, __fmaf_rn(r2.z, dy, __fmul_rn(r2.w, dz))) - r3.w;
-    const float s3 = __fmaf_rn(r3.x, dx, __fmaf_rn(r3.y, dy, __fmul_rn(r3.z, dz)));
-    const float ee = fmaxf(0.f, fmaxf(s1, fmaxf(s2, s3)));
-    return __fmaf_rn(hh, hh, __fmul_rn(ee, ee));
+__device__ __forceinline__ uint64_t add2_dn(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
 }
-__device__ __forceinline__ float lb2_vert(const float4* r, float qx, float qy, float qz) {
-    const float4 r0 = r[0], r4 = r[4], r5 = r[5];
-    const float dx = qx - r0.x, dy = qy - r0.y, dz = qz - r0.z;  // q - a
-    const float ex = qx - r4.x, ey = qy - r4.y, ez = qz - r4.z;  // q - b
-    const float gx = qx - r4.w, gy = qy - r5.x, gz = qz - r5.y;  // q - c
-    const float Da = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-    const float Db = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-    const float Dc = __fmaf_rn(gx, gx, __fmaf_rn(gy, gy, __fmul_rn(gz, gz)));
-    float mx = dx, my = dy, mz = dz, DV = Da;    // m = q - V, V the nearest vertex
-    if (Db < DV) { mx = ex; my = ey; mz = ez; DV = Db; }
-    if (Dc < DV) { mx = gx; my = gy; mz = gz; DV = Dc; }
-    const float ta = __fmaf_rn(mx, dx, __fmaf_rn(my, dy, __fmul_rn(mz, dz)));
-    const float tb = __fmaf_rn(mx, ex, __fmaf_rn(my, ey, __fmul_rn(mz, ez)));
-    const float tc = __fmaf_rn(mx, gx, __fmaf_rn(my, gy, __fmul_rn(mz, gz)));
-    const float tm = fminf(ta, fminf(tb, tc));   // <= DV (one term is m.m); <= 0 -> no information
-    return tm > 0.f ? __fdiv_rn(__fmul_rn(tm, tm), DV) : 0.f;
+__device__ __forceinline__ uint64_t sub2_up(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rp.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
 }
+__device__ __forceinline__ uint64_t mul2_dn(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t fma2_dn(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// ---- bounding-cylinder lower bound ------------------------------------------
+// A record {c, 4R^2}, {n, t} (p2m_engine.cu fit_cyl) encloses every member face: |nn.(x-c)| <= t and
+// in-plane distance <= R (nn = n/|n|).  For the fp32 query q_f, v = q_f - c, h = n.v, S = |v|^2:
+//   d(q_f, cylinder)^2 = a^2 + max(0, rho - R)^2,  a = max(0, |h| - t),  rho^2 = S - h^2.
+// The stored t already covers the fp32 error of |h| (40 * 2^-24 * M, M = max |coordinate| of D), and
+// rho^2 is lowered by kRhoErr * S, which covers the rounding of S and h^2; every later step rounds
+// toward the safe side, so "pruned" below implies d(q_f, cylinder) > U.  U is the row's d_min bound
+// (DK: rounded up, plus the fp32 rounding slack of q, times 1 + 1e-6), so a pruned face can neither
+// beat nor tie the row's (d^2, face id) minimum.  Square-free: with rho_lo > R,
+//   (rho - R)^2 + a^2 > U^2  <=>  B > 2 R rho,  B = rho^2 + R^2 + a^2 - U^2  <=>  B > 0 && B^2 > 4R^2 rho^2.
+// For one face (t ~ 0, R = its min-enclosing radius) this is the distance to its bounding disk: on
+// c5, 5 faces per query pass it against 334 for the bounding sphere (same final d_min).
+constexpr float kRhoErr = 24.0f / 16777216.0f;   // 24 * 2^-24
+
+// may some point of the cylinder lie within U of q_f (U2 = U^2 rounded up)?  false = prune
+__device__ __forceinline__ bool cyl_near(float qx, float qy, float qz, float U2, float4 c0, float4 c1) {
+    const float vx = qx - c0.x, vy = qy - c0.y, vz = qz - c0.z;
+    const float h = __fmaf_rn(vz, c1.z, __fmaf_rn(vy, c1.y, __fmul_rn(vx, c1.x)));
+    const float S = __fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx)));
+    const float rl = __fmaf_rn(S, -kRhoErr, __fmaf_rn(-h, h, S));   // <= rho^2
+    const float a = fmaxf(fabsf(h) - c1.w, 0.f);
+    const float A = __fmul_rd(a, a);
+    if (A > U2) return false;
+    if (4.f * rl > c0.w) {                                         // rho_lo > R
+        const float nB = __fsub_ru(U2, __fadd_rd(__fmaf_rd(c0.w, 0.25f, rl), A));   // >= -B
+        if (nB < 0.f && __fmul_rd(nB, nB) > __fmul_ru(c0.w, rl)) return false;
+    }
+    return true;
+}
+
+// visiting-order key: an (approximate) lower bound of d(q, cylinder)^2 as an ordered uint
+__device__ __forceinline__ uint32_t cyl_key(float qx, float qy, float qz, float4 c0, float4 c1) {
+    const float vx = qx - c0.x, vy = qy - c0.y, vz = qz - c0.z;
+    const float h = __fmaf_rn(vz, c1.z, __fmaf_rn(vy, c1.y, __fmul_rn(vx, c1.x)));
+    const float S = __fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx)));
+    const float a = fmaxf(fabsf(h) - c1.w, 0.f);
+    const float e = fmaxf(__fsqrt_rn(fmaxf(__fmaf_rn(-h, h, S), 0.f)) - 0.5f * __fsqrt_rn(c0.w), 0.f);
+    return __float_as_uint(__fmaf_rn(a, a, e * e));
+}
+
 // One CTA per tile (all rows share one site).  A tile of m rows uses G = ceil(m/32) warps per
 // replica and R = 8 / G replicas; replica r scans the 32-candidate batches b == r (mod R) of every
 // staged chunk, so small groups still keep all 8 warps busy.  Per batch, each lane computes a
-// pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
-// warp walks the union of set bits in list order; a lane whose bit is set applies the tight fp32
-// lower bound with its CURRENT d_min and, on pass, the exact point-triangle kernel on the face
-// record (all lanes read the same record: broadcast).  Every prune is conservative (DESIGN.md
-// section 9), so each row's result is the full-list argmin.  Replicas are merged by the
-// lexicographic min of (d^2, face id), the sequential argmin.
+// pass/prune bit per candidate with the conservative fp32 disk test (branch-free, f32x2), then the
+// warp walks the union of set bits in list order: a lane whose bit is set re-tests the disk with its
+// CURRENT d_min and, on pass, runs the exact point-triangle kernel on the face record (all lanes read
+// the same record: broadcast).  Every prune is conservative, so each row's
+// result is the full-list argmin.  Replicas are merged by the lexicographic min of (d^2, face id),
+// the sequential argmin.
 constexpr int kChunk = 256;
 constexpr int kWinChunks = 256;                  // level-0 need bits are computed per window of chunks
 static_assert(kWinChunks <= kTile, "one thread per window chunk when ordering");
 
 constexpr int kWarps = kTile / 32;
 
+// Staged disks of one 32-entry batch, pair-interleaved so that every 16-byte load yields two f32x2
+// operands: pair pp = candidates (2pp, 2pp+1) occupies 16 floats
+//   (cx0,cx1,cy0,cy1) (cz0,cz1,R4_0,R4_1) (nx0,nx1,ny0,ny1) (nz0,nz1,t0,t1)
+// stage_disk writes candidate k's record (r0 = {c, 4R^2}, r1 = {n, t}) into that layout.
+__device__ __forceinline__ void stage_disk(float* pf, int k, float4 r0, float4 r1) {
+    float* b = pf + 16 * (k >> 1) + (k & 1);
+    b[0] = r0.x; b[2] = r0.y; b[4] = r0.z; b[6] = r0.w;
+    b[8] = r1.x; b[10] = r1.y; b[12] = r1.z; b[14] = r1.w;
+}
+__device__ __forceinline__ void staged_disk(const float* pf, int k, float4& r0, float4& r1) {
+    const float* b = pf + 16 * (k >> 1) + (k & 1);
+    r0 = make_float4(b[0], b[2], b[4], b[6]);
+    r1 = make_float4(b[8], b[10], b[12], b[14]);
+}
 
-// One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)}, lb: 32 x
-// 64-byte lower-bound records, fid: 32 face ids), scanned for this lane's row.  Each lane computes a
-// pass/prune bit per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the
-// warp walks the union of set bits in list order; a lane whose bit is set applies the tight fp32
-// lower bound with its CURRENT d_min, and survivors run the exact fp64 kernel on the face record
-// (all lanes read the same record: broadcast).  (Re-testing the fp32 sphere first was measured
-// slower: the lower bound subsumes it.)  stage_lb: the lower-bound records of the
-// union are loaded here (lane k holds entry k's face id my_f).  Called by every lane of the warp.
+// One 32-entry batch staged in shared memory (disks: 16 pairs x 64 bytes, fid: 32 face ids), scanned
+// for this lane's row.  Called by every lane of the warp.
 template <bool kCounters>
 __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, const V& q, uint64_t QX, uint64_t QY,
                                                uint64_t QZ, uint64_t& DK, double& best, uint32_t& bf,
                                                uint32_t& exact, unsigned long long& passes,
                                                unsigned long long& rare_iters, unsigned long long& sbytes,
-                                               const float4* pair, float4* lb, const uint32_t* fid, int valid,
-                                               bool stage_lb, uint32_t my_f, int lane, float* sdk) {
+                                               const float4* disk, const uint32_t* fid, int valid, int lane,
+                                               float* sdk) {
     const float K = 1.000001f;
     const float delta = p.f32_delta;
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
@@ -253,23 +285,41 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         if (v < dkx) DK = pk2(v, v);
     }
     if (active) {
-#pragma unroll
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        const float u2 = __fmul_ru(dkx, dkx);
+        const uint64_t U2 = pk2(u2, u2);
+        const uint64_t NRHO = pk2(-kRhoErr, -kRhoErr), M4 = pk2(-4.f, -4.f), Q = pk2(0.25f, 0.25f);
+#pragma unroll 4
         for (int pp = 0; pp < 16; ++pp) {
-            const float4 A = pair[2 * pp], B = pair[2 * pp + 1];
-            const uint64_t dx = sub2(QX, pk2(A.x, A.y));
-            const uint64_t dy = sub2(QY, pk2(A.z, A.w));
-            const uint64_t dz = sub2(QZ, pk2(B.x, B.y));
-            const uint64_t d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-            const uint64_t th = add2_up(pk2(B.z, B.w), DK);
-            const uint64_t t2 = mul2_up(th, th);
-            // prune iff d2 > t2, i.e. iff fl(t2 - d2) is negative: IEEE subtraction keeps the
-            // sign of the exact difference and gives +0 on equality (pass), and NaN from
-            // inf - inf (padding against an unset d_min) has its sign bit clear (pass, masked
-            // by valid) -- so one FADD2 and two funnel shifts collect the 32 prune bits
-            float x0, x1;
-            upk2(sub2(t2, d2), x0, x1);
-            mask = __funnelshift_l(__float_as_uint(x0), mask, 1);
-            mask = __funnelshift_l(__float_as_uint(x1), mask, 1);
+            const float4 A0 = disk[4 * pp], A1 = disk[4 * pp + 1], A2 = disk[4 * pp + 2], A3 = disk[4 * pp + 3];
+            const uint64_t vx = sub2(QX, pk2(A0.x, A0.y));
+            const uint64_t vy = sub2(QY, pk2(A0.z, A0.w));
+            const uint64_t vz = sub2(QZ, pk2(A1.x, A1.y));
+            const uint64_t h = fma2(vz, pk2(A3.x, A3.y), fma2(vy, pk2(A2.z, A2.w), mul2(vx, pk2(A2.x, A2.y))));
+            const uint64_t S = fma2(vz, vz, fma2(vy, vy, mul2(vx, vx)));
+            const uint64_t rl = fma2(S, NRHO, sub2(S, mul2(h, h)));        // <= rho^2
+            float h0, h1;
+            upk2(h, h0, h1);
+            const float a0 = fmaxf(fabsf(h0) - A3.z, 0.f), a1 = fmaxf(fabsf(h1) - A3.w, 0.f);
+            const uint64_t a = pk2(a0, a1);
+            const uint64_t AA = mul2_dn(a, a);
+            const uint64_t R4 = pk2(A1.z, A1.w);
+            const uint64_t n1 = sub2(U2, AA);                             // < 0 iff a^2 > U^2
+            const uint64_t n2 = fma2(rl, M4, R4);                         // < 0 iff rho_lo > R
+            const uint64_t nB = sub2_up(U2, add2_dn(fma2_dn(R4, Q, rl), AA));   // < 0 => B > 0
+            const uint64_t n4 = sub2(mul2_up(R4, rl), mul2_dn(nB, nB));   // < 0 iff B^2 > 4 R^2 rho^2
+            float x1a, x1b, x2a, x2b, xBa, xBb, x4a, x4b;
+            upk2(n1, x1a, x1b);
+            upk2(n2, x2a, x2b);
+            upk2(nB, xBa, xBb);
+            upk2(n4, x4a, x4b);
+            // prune bit = sign(n1) | (sign(n2) & sign(nB) & sign(n4)) (IEEE: an exact zero difference
+            // is +0 and never prunes; NaN from inf - inf has its sign bit clear)
+            const uint32_t pa = __float_as_uint(x1a) | (__float_as_uint(x2a) & __float_as_uint(xBa) & __float_as_uint(x4a));
+            const uint32_t pb = __float_as_uint(x1b) | (__float_as_uint(x2b) & __float_as_uint(xBb) & __float_as_uint(x4b));
+            mask = __funnelshift_l(pa, mask, 1);
+            mask = __funnelshift_l(pb, mask, 1);
         }
         mask = ~__brev(mask);  // bit k = candidate k passes
         if (valid < 32) mask &= (1u << valid) - 1u;
@@ -277,29 +327,17 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
     uint32_t um = __reduce_or_sync(0xffffffffu, mask);
     if (kCounters) {
         passes += __popc(mask);
-        if (lane == 0) {
-            rare_iters += 32u * __popc(um);
-            if (stage_lb) sbytes += 16ull * kLbRec * __popc(um);  // the union's lower-bound records
-        }
+        if (lane == 0) rare_iters += 32u * __popc(um);
     }
-    if (stage_lb && um) {
-        if ((um >> lane) & 1u) {
-            const float4* lr = p.lbr + kLbRec * (uint64_t)my_f;
-#pragma unroll
-            for (int k = 0; k < kLbRec; ++k) lb[kLbRec * lane + k] = lr[k];
-        }
-        __syncwarp();
-    }
-    // the exact test of one candidate kk of this lane: the tight lower bound against the CURRENT
-    // d_min (the batch mask used the d_min of the batch start), then fp64
+    // the exact test of one candidate kk of this lane: the disk again with the CURRENT d_min (the batch
+    // mask used the d_min of the batch start), then fp64
     auto visit = [&](int kk) -> bool {
         {
             float dkx, dky;
             upk2(DK, dkx, dky);
-            const float thl = __fmul_ru(__fadd_ru(dkx, p.lb_margin), 1.000001f);
-            const float th2 = __fmul_ru(thl, thl);
-            if (lb2_plane(lb + kLbRec * kk, qxf, qyf, qzf) > th2) return false;
-            if (lb2_vert(lb + kLbRec * kk, qxf, qyf, qzf) > th2) return false;
+            float4 r0, r1;
+            staged_disk(reinterpret_cast<const float*>(disk), kk, r0, r1);
+            if (!cyl_near(qxf, qyf, qzf, __fmul_ru(dkx, dkx), r0, r1)) return false;
         }
         const uint32_t f = fid[kk];
         V a, bb3, c3, pp3;
@@ -329,7 +367,6 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         if ((mask >> kk) & 1u) ex = visit(kk);
         if (kCounters && __any_sync(0xffffffffu, ex) && lane == 0) sbytes += 96;  // one face record per warp visit
     }
-
 }
 
 // d_min seeds of one row of site s (both are upper bounds of the distance to the mesh, so the
@@ -357,27 +394,27 @@ __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q
         }
     }
     if (!p.no_seed && !p.no_batch) {
-        // Tighter seed: every face of a batch/chunk lies within |q - C| + R of q, so the min of that
-        // over the list's spheres bounds the distance to the mesh from above.  fp32 with upward
-        // rounding: sqrt(d2f)*(1+1e-6) covers the rounding of d2f, delta the fp32 rounding of q
-        // (C is an exact float), and the stored radius is R*K rounded up (>= R).  The min runs over
-        // every chunk sphere, then over the batch spheres of this lane's best chunk.
+        // Tighter seed: every chunk and batch carries a point P on the mesh near its centre
+        // (p2m_engine.cu group_point), so |q - P| bounds the distance to the mesh from above.  fp32
+        // with upward rounding: sqrt(d2f)*(1+1e-6) covers the rounding of d2f, delta the fp32
+        // rounding of q and of P.  The min runs over every chunk point, then over the batch points
+        // of this lane's best chunk.
         float ub = finf;
         uint32_t bc = 0;
         for (uint32_t c2 = 0; c2 < nch; ++c2) {
-            const float4 c = p.csph[co + c2];  // same address across the tile's lanes: broadcast
+            const float4 c = p.cpt[co + c2];  // same address across the tile's lanes: broadcast
             const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
             const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            const float u = __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w);
+            const float u = __fmul_ru(__fsqrt_ru(d2f), 1.000001f);
             if (u < ub) { ub = u; bc = c2; }
         }
         const uint64_t nbl = p.boff[s + 1] - bo;
         const uint64_t bb0 = (uint64_t)bc * (kChunk / 32), bb1 = min(nbl, bb0 + kChunk / 32);
         for (uint64_t b2 = bb0; b2 < bb1; ++b2) {
-            const float4 c = p.bsph[bo + b2];
+            const float4 c = p.bpt[bo + b2];
             const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
             const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            ub = fminf(ub, __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), c.w));
+            ub = fminf(ub, __fmul_ru(__fsqrt_ru(d2f), 1.000001f));
         }
         ub = __fadd_ru(ub, delta);
         if ((double)ub < dmin) {
@@ -407,16 +444,14 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                                                         const uint32_t* __restrict__ tiles,
                                                         const uint32_t* __restrict__ meta,
                                                         const uint32_t* __restrict__ order, Out o) {
-    __shared__ float4 s_pair[kWarps][32];
+    __shared__ float4 s_disk[kWarps][64];
     __shared__ uint32_t s_fid[kWarps][32];
-    __shared__ float4 s_lb[kWarps][32 * kLbRec];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t nt = meta[0], ns = meta[2];
     const uint32_t ti = blockIdx.x * kWarps + w;
     if (ti >= ns) return;                        // warp-uniform: no block barrier in this kernel
-    float4* wp = s_pair[w];
+    float4* wd = s_disk[w];
     uint32_t* wf = s_fid[w];
-    float4* wl = s_lb[w];
     const uint32_t b = order[nt - ns + ti];
     const uint32_t start = tiles[b];
     const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
@@ -444,26 +479,18 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     const uint64_t bo = p.boff[s], co = p.coff[s];
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
-    if (kCounters && lane == 0) sbytes += 16ull * nch + 76;  // chunk spheres, site ref, offsets, tile meta
-    // conservative "may some member be within d_min" test of this lane's row against a group sphere
-    auto near = [&](float4 c) {
+    if (kCounters && lane == 0) sbytes += 48ull * nch + 76;  // chunk spheres + cylinders, site ref, offsets, tile meta
+    // conservative "may some member be within d_min" test of this lane's row against a group cylinder
+    auto near = [&](float4 c0, float4 c1) {
         float dkx, dky;
         upk2(DK, dkx, dky);
-        const float dx = fx - c.x, dy = fy - c.y, dz = fz - c.z;
-        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-        const float th = __fadd_ru(c.w, dkx);
-        return !(d2f > __fmul_ru(th, th));
-    };
-    auto lbkey = [&](float4 c) {                 // lower bound for the first row, as an ordered key
-        const float dx = rx - c.x, dy = ry - c.y, dz = rz - c.z;
-        const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
-        return __float_as_uint(fmaxf(lb, 0.f));
+        return cyl_near(fx, fy, fz, __fmul_ru(dkx, dkx), c0, c1);
     };
     // chunks best-first (<= 4: every lane ranks them identically)
     uint32_t ck[kSmallChunks], ci[kSmallChunks];
 #pragma unroll
     for (uint32_t c = 0; c < kSmallChunks; ++c) {
-        ck[c] = c < nch ? (nch > 1 ? lbkey(p.csph[co + c]) : 0u) : 0xffffffffu;
+        ck[c] = c < nch ? (nch > 1 ? cyl_key(rx, ry, rz, p.ccy[kCy * (co + c)], p.ccy[kCy * (co + c) + 1]) : 0u) : 0xffffffffu;
         ci[c] = c;
     }
 #pragma unroll
@@ -474,19 +501,23 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                 const uint32_t tk = ck[j]; ck[j] = ck[j - 1]; ck[j - 1] = tk;
                 const uint32_t tc = ci[j]; ci[j] = ci[j - 1]; ci[j - 1] = tc;
             }
-    float* wpf = reinterpret_cast<float*>(wp);
+    float* wdf = reinterpret_cast<float*>(wd);
     for (uint32_t oc = 0; oc < nch; ++oc) {
         const uint32_t cidx = ci[oc];
-        if (nch > 1 && !p.no_batch && !__any_sync(0xffffffffu, active && near(p.csph[co + cidx]))) continue;
+        if (nch > 1 && !p.no_batch &&
+            !__any_sync(0xffffffffu, active && near(p.ccy[kCy * (co + cidx)], p.ccy[kCy * (co + cidx) + 1])))
+            continue;
         const uint64_t cb = beg + (uint64_t)cidx * kChunk;
         const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
-        if (kCounters && lane == 0) sbytes += 16ull * nb;  // the chunk's batch spheres
+        if (kCounters && lane == 0) sbytes += 32ull * nb;  // the chunk's batch cylinders
         // the chunk's batches best-first for the first row
-        float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 b0c = make_float4(0.f, 0.f, 0.f, 0.f), b1c = b0c;
         uint32_t bk = 0xffffffffu;
         if (lane < nb) {
-            bs = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + lane];
-            bk = lbkey(bs);
+            const uint64_t gi = kCy * (bo + (uint64_t)cidx * (kChunk / 32) + lane);
+            b0c = p.bcy[gi];
+            b1c = p.bcy[gi + 1];
+            bk = cyl_key(rx, ry, rz, b0c, b1c);
         }
         uint32_t rk = 0;
 #pragma unroll
@@ -496,26 +527,22 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
         }
         for (int pos = 0; pos < nb; ++pos) {
             const int src = __ffs(__ballot_sync(0xffffffffu, lane < nb && rk == (uint32_t)pos)) - 1;
-            const float4 c = make_float4(__shfl_sync(0xffffffffu, bs.x, src), __shfl_sync(0xffffffffu, bs.y, src),
-                                         __shfl_sync(0xffffffffu, bs.z, src), __shfl_sync(0xffffffffu, bs.w, src));
-            if (!p.no_batch && !__any_sync(0xffffffffu, active && near(c))) continue;  // pruned whole
+            const float4 c0 = make_float4(__shfl_sync(0xffffffffu, b0c.x, src), __shfl_sync(0xffffffffu, b0c.y, src),
+                                          __shfl_sync(0xffffffffu, b0c.z, src), __shfl_sync(0xffffffffu, b0c.w, src));
+            const float4 c1 = make_float4(__shfl_sync(0xffffffffu, b1c.x, src), __shfl_sync(0xffffffffu, b1c.y, src),
+                                          __shfl_sync(0xffffffffu, b1c.z, src), __shfl_sync(0xffffffffu, b1c.w, src));
+            if (!p.no_batch && !__any_sync(0xffffffffu, active && near(c0, c1))) continue;  // pruned whole
             const uint64_t b0 = cb + 32ull * src;
             const int valid = (int)min((uint64_t)32, end - b0);
             uint32_t f = 0;
-            float4 rv = make_float4(finf, 0.f, 0.f, 0.f);
-            if (lane < valid) { f = p.lfs[b0 + lane]; rv = p.f32[f]; }
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+            if (lane < valid) { f = p.lfs[b0 + lane]; r0 = p.fcy[kCy * (uint64_t)f]; r1 = p.fcy[kCy * (uint64_t)f + 1]; }
             wf[lane] = f;
-            {
-                const int pp = lane >> 1, h = lane & 1;
-                wpf[8 * pp + h] = rv.x;
-                wpf[8 * pp + 2 + h] = rv.y;
-                wpf[8 * pp + 4 + h] = rv.z;
-                wpf[8 * pp + 6 + h] = rv.w;
-            }
+            stage_disk(wdf, lane, r0, r1);
             __syncwarp();
-            if (kCounters && lane == 0) sbytes += 20ull * valid;  // staged ids + fp32 records
+            if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
             scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      wp, wl, wf, valid, true, f, lane, nullptr);
+                                      wd, wf, valid, lane, nullptr);
             __syncwarp();                        // the slice is rewritten by the next batch
         }
     }
@@ -562,13 +589,13 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
 
 
 #ifndef P2M_EARLY1
-#define P2M_EARLY1 2  // single-chunk CTA tiles: chunk loads issued before the seeds (cp.async spheres; 2: + records)
+#define P2M_EARLY1 1  // single-chunk CTA tiles: chunk loads issued before the seeds (cp.async batch cylinders)
 #endif
 #ifndef P2M_BATCH_ORDER
 #define P2M_BATCH_ORDER 1   // block path: visit a chunk's batches best-first for the tile's first row
 #endif
 #ifndef P2M_SCAN_MINB
-#define P2M_SCAN_MINB 4  // resident CTAs per SM the register budget is sized for (measured: 4 > 3 > 2)
+#define P2M_SCAN_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 template <bool kCounters>
 __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, const double* __restrict__ q_xyz,
@@ -577,10 +604,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                                                          const uint32_t* __restrict__ tiles,
                                                          const uint32_t* __restrict__ meta,
                                                          const uint32_t* __restrict__ order, Out o) {
-    __shared__ float4 s_pair[kChunk];            // pairs: (x0,x1,y0,y1), (z0,z1,rk0,rk1)
+    __shared__ float4 s_disk[2 * kChunk];        // the chunk's face disks, pair-interleaved (stage_disk)
     __shared__ uint32_t s_fid[kChunk];
-    __shared__ float4 s_lb[kChunk * kLbRec];     // the chunk's fp32 lower-bound records (96 B each)
-    __shared__ float4 s_bsph[kChunk / 32];       // the chunk's batch spheres (fp32, conservative)
+    __shared__ float4 s_bcy[kCy * (kChunk / 32)];  // the chunk's batch cylinders
     __shared__ uint32_t s_need;                  // batches some warp of the CTA must scan
     __shared__ uint32_t s_cw[kWinChunks / 32];   // chunks of the current window some row must scan
     __shared__ uint32_t s_oidx[kWinChunks];      // ... in visiting order
@@ -617,8 +643,6 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         QX = pk2(fx, fx); QY = pk2(fy, fy); QZ = pk2(fz, fz);
         if (tid == 0) s_qrep = make_float4(fx, fy, fz, 0.f);
     }
-    const float K = 1.000001f;
-    const float delta = p.f32_delta;
     const float finf = __int_as_float(0x7f800000);
     double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
     uint64_t DK = pk2(finf, finf);               // (dmin_up + delta) * K, rounded up, both halves
@@ -627,29 +651,29 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
     unsigned long long sbytes = 0;               // structure bytes loaded (counters mode; bench roofline)
     const uint64_t beg = p.off[s], end = p.off[s + 1];
-    float* s_pf = reinterpret_cast<float*>(s_pair);
-    const uint64_t bo = p.boff[s];               // this list's first 32-entry batch sphere
-    const uint64_t co = p.coff[s];               // ... and first 256-entry chunk sphere
+    float* s_df = reinterpret_cast<float*>(s_disk);
+    const uint64_t bo = p.boff[s];               // this list's first 32-entry batch
+    const uint64_t co = p.coff[s];               // ... and first 256-entry chunk
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
-    if (kCounters && tid == 0) sbytes += 16ull * nch + 76;  // chunk spheres, site ref, offsets, tile meta
+    if (kCounters && tid == 0) sbytes += 48ull * nch + 76;  // chunk spheres + cylinders, site ref, offsets, tile meta
 #define qxf __uint_as_float((uint32_t)QX)
 #define qyf __uint_as_float((uint32_t)QY)
 #define qzf __uint_as_float((uint32_t)QZ)
-    // register prefetch of one chunk entry per thread: face id + its 16-byte fp32 pre-filter record
+    // register prefetch of one chunk entry per thread: face id + its disk record
     uint32_t nf = 0;
-    float4 nv = make_float4(finf, 0.f, 0.f, 0.f);
-    uint32_t pre_c = 0xffffffffu;                // chunk held in (nf, nv)
+    float4 nv0 = make_float4(0.f, 0.f, 0.f, 0.f), nv1 = nv0;
+    uint32_t pre_c = 0xffffffffu;                // chunk held in (nf, nv0, nv1)
     bool first_chunk = true;
 #if P2M_EARLY1
     const bool early = nch == 1 && G > 1;        // the one chunk of a single-chunk CTA tile: its loads
     if (early) {                                 // start now and land during the seed computation
         const int mc0 = (int)min((uint64_t)kChunk, end - beg);
-        if (tid < ((mc0 + 31) >> 5)) {           // batch spheres: async copy to shared, no registers
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_bsph[tid]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(p.bsph + bo + tid));
-            asm volatile("cp.async.commit_group;");
+        if (tid < kCy * ((mc0 + 31) >> 5)) {     // batch cylinders: async copy to shared, no registers
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_bcy[tid]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(p.bcy + kCy * bo + tid));
         }
-        if (tid < mc0) { nf = p.lfs[beg + tid]; nv = p.f32[nf]; }
+        asm volatile("cp.async.commit_group;");
+        if (tid < mc0) { nf = p.lfs[beg + tid]; nv0 = p.fcy[kCy * (uint64_t)nf]; nv1 = p.fcy[kCy * (uint64_t)nf + 1]; }
         pre_c = 0;
     }
 #endif
@@ -667,22 +691,15 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             if (v < dkx) DK = pk2(v, v);
         }
     };
-#if P2M_EARLY1 >= 2
-    if (early && tid < (int)min((uint64_t)kChunk, end - beg)) {
-        // the chunk's lower-bound records, async into shared memory (nf has landed by now); waited
-        // for just before the staging barrier
-        const float4* lr = p.lbr + kLbRec * (uint64_t)nf;
-        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&s_lb[kLbRec * tid]);
-#pragma unroll
-        for (int k = 0; k < kLbRec; ++k)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa + 16 * k), "l"(lr + k));
-    }
-    asm volatile("cp.async.commit_group;");
-#endif
+    auto near = [&](float4 c0, float4 c1) {      // conservative: may a member of the group be within d_min?
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        return cyl_near(qxf, qyf, qzf, __fmul_ru(dkx, dkx), c0, c1);
+    };
     for (uint32_t w0 = 0; w0 < nch; w0 += kWinChunks) {
         const uint32_t wn = min(nch - w0, (uint32_t)kWinChunks);
         const int nwords = (int)((wn + 31) >> 5);
-        // level 0: a chunk is scanned only if some row's conservative bound to its sphere does not
+        // level 0: a chunk is scanned only if some row's conservative bound to its cylinder does not
         // exceed that row's d_min (any replica's d_min is a valid upper bound of the row's distance)
         // a single-chunk list (most tiles) has a trivial window: no votes, no ordering, no barriers
         int nord = 1;
@@ -691,24 +708,16 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             if (tid < kWinChunks / 32) {
                 const int nv_ = min(32, max(0, (int)wn - 32 * tid));
                 const uint32_t vmask = nv_ == 32 ? 0xffffffffu : ((1u << nv_) - 1u);
-                s_cw[tid] = (p.no_batch || nch == 1) ? vmask : 0u;
+                s_cw[tid] = p.no_batch ? vmask : 0u;
             }
             __syncthreads();
-            if (warp_on && !p.no_batch && nch > 1) {
-                float dkx, dky;
-                upk2(DK, dkx, dky);
+            if (warp_on && !p.no_batch) {
                 for (int wi = r; wi < nwords; wi += R) {
                     uint32_t bits = 0;
                     const int kn = min(32, (int)wn - 32 * wi);
                     for (int k = 0; k < kn; ++k) {
-                        bool need = false;
-                        if (active) {
-                            const float4 c = p.csph[co + w0 + 32 * wi + k];
-                            const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
-                            const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                            const float th = __fadd_ru(c.w, dkx);
-                            need = !(d2f > __fmul_ru(th, th));
-                        }
+                        const uint64_t gi = kCy * (co + w0 + 32 * wi + k);
+                        const bool need = active && near(p.ccy[gi], p.ccy[gi + 1]);
                         if (__any_sync(0xffffffffu, need)) bits |= 1u << k;
                     }
                     if (lane == 0 && bits) atomicOr(&s_cw[wi], bits);
@@ -720,24 +729,20 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             // level.  The order changes neither the (d^2, face id) argmin nor which faces may be skipped.
             {
                 int pos = -1;
-                uint32_t key = 0;
+                uint32_t okey = 0;
                 if (tid < (int)wn) {
                     const uint32_t wb = s_cw[tid >> 5];
                     if ((wb >> (tid & 31)) & 1u) {
                         pos = __popc(wb & ((1u << (tid & 31)) - 1u));
                         for (int k = 0; k < (tid >> 5); ++k) pos += __popc(s_cw[k]);
-                        if (nch > 1) {
-                            const float4 c = p.csph[co + w0 + tid];
-                            const float4 qr = s_qrep;
-                            const float dx = qr.x - c.x, dy = qr.y - c.y, dz = qr.z - c.z;
-                            const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
-                            key = __float_as_uint(fmaxf(lb, 0.f));
-                        }
+                        const uint64_t gi = kCy * (co + w0 + tid);
+                        const float4 qr = s_qrep;
+                        okey = cyl_key(qr.x, qr.y, qr.z, p.ccy[gi], p.ccy[gi + 1]);
                     }
                 }
                 nord = 0;
                 for (int k = 0; k < nwords; ++k) nord += __popc(s_cw[k]);
-                if (pos >= 0) { s_oidx[pos] = (uint32_t)tid; s_okey[pos] = key; }
+                if (pos >= 0) { s_oidx[pos] = (uint32_t)tid; s_okey[pos] = okey; }
                 __syncthreads();
                 if (nord > 1) {
                     uint32_t mi = 0, rank = 0;
@@ -755,17 +760,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 }
             }
         }
-        // One 32-entry batch staged in shared memory (pair: 16 x {(x0,x1,y0,y1),(z0,z1,rk0,rk1)},
-        // lb: 32 x 64-byte lower-bound records, fid: 32 face ids).  Each lane computes a pass/prune bit
-        // per candidate with the conservative fp32 pre-filter (branch-free, f32x2), then the warp
-        // walks the union of set bits in list order; a lane whose bit is set applies the tight fp32
-        // lower bound with its CURRENT d_min, and survivors run the exact fp64 kernel on the face
-        // record (all lanes read the same record: broadcast).  stage_lb: the lower-bound
-        // records of the union are loaded here (lane k holds entry k's face id my_f).
-        auto scan_batch = [&](const float4* pair, float4* lb, const uint32_t* fid, int valid, bool stage_lb,
-                              uint32_t my_f) {
+        auto scan_batch = [&](const float4* disk, const uint32_t* fid, int valid) {
             scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      pair, lb, fid, valid, stage_lb, my_f, lane, R > 1 && active ? &s_dk[j] : nullptr);
+                                      disk, fid, valid, lane, R > 1 && active ? &s_dk[j] : nullptr);
         };
         if (G == 1) {
             // Small tile (<= 32 rows): every warp holds all rows, so each batch needs only one warp.
@@ -775,10 +772,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             if (tid == 0) s_next = 0u;
             __syncthreads();
             const uint32_t T = (uint32_t)nord * (kChunk / 32);
-            float4* wp = s_pair + 32 * w;
-            float* wpf = reinterpret_cast<float*>(wp);
+            float4* wd = s_disk + 64 * w;
+            float* wdf = reinterpret_cast<float*>(wd);
             uint32_t* wf = s_fid + 32 * w;
-            float4* wl = s_lb + 32 * kLbRec * w;
             for (;;) {
                 uint32_t t = 0;
                 if (lane == 0) t = atomicAdd(&s_next, 1u);
@@ -791,31 +787,17 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 const int valid = (int)min((uint64_t)32, end - b0);
                 bool need = p.no_batch != 0;
                 refresh_dk();
-                if (active && !need) {
-                    const float4 c = p.bsph[bo + gb];
-                    float dkx, dky;
-                    upk2(DK, dkx, dky);
-                    const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
-                    const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                    const float th = __fadd_ru(c.w, dkx);
-                    need = !(d2f > __fmul_ru(th, th));
-                }
-                if (kCounters && lane == 0) sbytes += 16;  // the batch sphere
-                if (!__any_sync(0xffffffffu, need)) continue;  // pruned whole by its batch sphere
-                if (kCounters && lane == 0) sbytes += 20ull * valid;  // staged ids + fp32 records
+                if (active && !need) need = near(p.bcy[kCy * (bo + gb)], p.bcy[kCy * (bo + gb) + 1]);
+                if (kCounters && lane == 0) sbytes += 32;  // the batch cylinder
+                if (!__any_sync(0xffffffffu, need)) continue;  // pruned whole by its batch cylinder
+                if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
                 uint32_t f = 0;
-                float4 rv = make_float4(finf, 0.f, 0.f, 0.f);
-                if (lane < valid) { f = p.lfs[b0 + lane]; rv = p.f32[f]; }
+                float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+                if (lane < valid) { f = p.lfs[b0 + lane]; r0 = p.fcy[kCy * (uint64_t)f]; r1 = p.fcy[kCy * (uint64_t)f + 1]; }
                 wf[lane] = f;
-                {
-                    const int pp = lane >> 1, h = lane & 1;
-                    wpf[8 * pp + h] = rv.x;
-                    wpf[8 * pp + 2 + h] = rv.y;
-                    wpf[8 * pp + 4 + h] = rv.z;
-                    wpf[8 * pp + 6 + h] = rv.w;
-                }
+                stage_disk(wdf, lane, r0, r1);
                 __syncwarp();
-                scan_batch(wp, wl, wf, valid, true, f);
+                scan_batch(wd, wf, valid);
                 __syncwarp();                    // the slice is rewritten by the next batch
             }
             continue;                            // next window (its first barrier orders s_next)
@@ -829,24 +811,21 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             first_chunk = false;
             if (pre_c != cidx) {
                 nf = 0;
-                nv = make_float4(finf, 0.f, 0.f, 0.f);
-                if (tid < mc) { nf = p.lfs[base + tid]; nv = p.f32[nf]; }
+                nv0 = make_float4(0.f, 0.f, 0.f, 0.f);
+                nv1 = nv0;
+                if (tid < mc) { nf = p.lfs[base + tid]; nv0 = p.fcy[kCy * (uint64_t)nf]; nv1 = p.fcy[kCy * (uint64_t)nf + 1]; }
             }
-            // level 1: the enclosing sphere of each 32-entry batch.  If every lane's conservative fp32
-            // bound to it exceeds the lane's d_min, every member sphere's bound does too, so the whole
+            // level 1: the enclosing cylinder of each 32-entry batch.  If every lane's conservative
+            // bound to it exceeds the lane's d_min, every member face's bound does too, so the whole
             // batch is pruned exactly as the per-candidate tests would prune it (and is never staged).
 #if P2M_EARLY1
             if (early) {
-#if P2M_EARLY1 >= 2
-                if (tid < nb) asm volatile("cp.async.wait_group 1;" ::: "memory");  // spheres, not the records
-#else
-                if (tid < nb) asm volatile("cp.async.wait_all;" ::: "memory");
-#endif
-            } else if (tid < nb) {
-                s_bsph[tid] = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + tid];
+                asm volatile("cp.async.wait_all;" ::: "memory");
+            } else if (tid < kCy * nb) {
+                s_bcy[tid] = p.bcy[kCy * (bo + (uint64_t)cidx * (kChunk / 32)) + tid];
             }
 #else
-            if (tid < nb) s_bsph[tid] = p.bsph[bo + (uint64_t)cidx * (kChunk / 32) + tid];
+            if (tid < kCy * nb) s_bcy[tid] = p.bcy[kCy * (bo + (uint64_t)cidx * (kChunk / 32)) + tid];
 #endif
             if (tid == 0) s_need = 0u;
             __syncthreads();
@@ -855,25 +834,17 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             if (warp_on) {
                 for (int bb = r; bb < nb; bb += R) {
                     bool need = p.no_batch != 0;
-                    if (active && !need) {
-                        const float4 c = s_bsph[bb];
-                        float dkx, dky;
-                        upk2(DK, dkx, dky);
-                        const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
-                        const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-                        const float th = __fadd_ru(c.w, dkx);
-                        need = !(d2f > __fmul_ru(th, th));
-                    }
+                    if (active && !need) need = near(s_bcy[kCy * bb], s_bcy[kCy * bb + 1]);
                     if (__any_sync(0xffffffffu, need)) wneed |= 1u << bb;
                 }
                 if (lane == 0 && wneed) atomicOr(&s_need, wneed);
             }
             __syncthreads();
             const uint32_t cneed = s_need;
-            if (kCounters && tid == 0) {         // ids + fp32 records + batch spheres, needed lb records
-                sbytes += 20ull * mc + 16ull * nb;
+            if (kCounters && tid == 0) {         // ids + disks of the needed batches, batch cylinders
+                sbytes += 32ull * nb;
                 for (int bb = 0; bb < nb; ++bb)
-                    if ((cneed >> bb) & 1u) sbytes += 16ull * kLbRec * min(32, mc - 32 * bb);
+                    if ((cneed >> bb) & 1u) sbytes += 36ull * min(32, mc - 32 * bb);
             }
             // prefetch the window's next chunk while this one is scanned
             auto prefetch_next = [&]() {
@@ -882,8 +853,9 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                     const uint32_t c2 = w0 + (nch > 1 ? s_oidx[oi + 1] : 0u);
                     const uint64_t b2 = beg + (uint64_t)c2 * kChunk;
                     nf = 0;
-                    nv = make_float4(finf, 0.f, 0.f, 0.f);
-                    if (b2 + tid < end) { nf = p.lfs[b2 + tid]; nv = p.f32[nf]; }
+                    nv0 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    nv1 = nv0;
+                    if (b2 + tid < end) { nf = p.lfs[b2 + tid]; nv0 = p.fcy[kCy * (uint64_t)nf]; nv1 = p.fcy[kCy * (uint64_t)nf + 1]; }
                     pre_c = c2;
                 }
             };
@@ -893,52 +865,34 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             }
             if (P2M_BATCH_ORDER && w == 0) {
                 // the chunk's batches best-first for the tile's first row (all rows share a cell)
-                uint32_t key = 0xffffffffu;
+                uint32_t bkey = 0xffffffffu;
                 if (lane < nb) {
-                    const float4 c = s_bsph[lane];
                     const float4 qr = s_qrep;
-                    const float dx = qr.x - c.x, dy = qr.y - c.y, dz = qr.z - c.z;
-                    const float lb = __fsqrt_rn(__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)))) - c.w;
-                    key = __float_as_uint(fmaxf(lb, 0.f));
+                    bkey = cyl_key(qr.x, qr.y, qr.z, s_bcy[kCy * lane], s_bcy[kCy * lane + 1]);
                 }
                 uint32_t rk = 0;
 #pragma unroll
-                for (int j = 0; j < kChunk / 32; ++j) {
-                    const uint32_t kj = __shfl_sync(0xffffffffu, key, j);
-                    rk += (kj < key || (kj == key && j < lane)) ? 1u : 0u;
+                for (int jj = 0; jj < kChunk / 32; ++jj) {
+                    const uint32_t kj = __shfl_sync(0xffffffffu, bkey, jj);
+                    rk += (kj < bkey || (kj == bkey && jj < lane)) ? 1u : 0u;
                 }
                 if (lane < nb) s_bord[rk] = (uint8_t)lane;
             }
-            {
-                const int pp = tid >> 1, h = tid & 1;
-                if (tid >= mc) nv = make_float4(finf, 0.f, 0.f, 0.f);  // never-passing pad (masked anyway)
+            if ((cneed >> (tid >> 5)) & 1u) {    // stage the needed batches: face ids + disks
                 s_fid[tid] = nf;
-#if P2M_EARLY1 >= 2
-                if (early) asm volatile("cp.async.wait_all;" ::: "memory");  // records copied at tile start
-                else
-#endif
-                if (tid < mc && ((cneed >> (tid >> 5)) & 1u)) {  // stage the lower-bound record (rare path, broadcast)
-                    const float4* lr = p.lbr + kLbRec * (uint64_t)nf;
-#pragma unroll
-                    for (int k = 0; k < kLbRec; ++k) s_lb[kLbRec * tid + k] = lr[k];
-                }
-                s_pf[8 * pp + h] = nv.x;
-                s_pf[8 * pp + 2 + h] = nv.y;
-                s_pf[8 * pp + 4 + h] = nv.z;
-                s_pf[8 * pp + 6 + h] = nv.w;
+                stage_disk(s_df, tid, nv0, nv1);
             }
             __syncthreads();
             prefetch_next();
             if (!warp_on) continue;
             for (int pos = r; pos < nb; pos += R) {
                 const int bb = P2M_BATCH_ORDER ? (int)s_bord[pos] : pos;
-                // pruned whole by its batch sphere for every row (cneed: the union over the replicas'
+                // pruned whole by its batch cylinder for every row (cneed: the union over the replicas'
                 // level-1 votes -- with the reordering a replica scans batches another one voted on).
                 // Without replicas each warp voted on every batch for its own rows: a batch its own
                 // vote pruned stays pruned (d_min only shrinks), so it is skipped too.
                 if (!(((R == 1 ? wneed : cneed) >> bb) & 1u)) continue;
-                const int k0 = bb * 32;
-                scan_batch(s_pair + k0, s_lb + kLbRec * k0, s_fid + k0, mc - k0, false, 0u);
+                scan_batch(s_disk + 64 * bb, s_fid + 32 * bb, mc - 32 * bb);
             }
         }
     }

@@ -37,6 +37,11 @@ for lo, hi in [(1, 8), (8, 32), (32, 64), (64, 128), (128, 256), (256, 257)]:
     m = (rows >= lo) & (rows < hi)
     print(f"  rows [{lo},{hi}): tiles {m.sum():6d}  CTA-ms {ms[m].sum():8.1f}  mean {ms[m].mean()*1e3 if m.any() else 0:7.1f} us")
 L_ = t[:, 2]
-for lo, hi in [(0, 256), (256, 1024), (1024, 4096), (4096, 1 << 40)]:
+for lo, hi in [(0, 256), (256, 1024), (1024, 4096), (4096, 16384), (16384, 65536), (65536, 1 << 40)]:
     m = (L_ >= lo) & (L_ < hi)
-    print(f"  list [{lo},{hi}): tiles {m.sum():6d}  CTA-ms {ms[m].sum():8.1f}")
+    print(f"  list [{lo},{hi}): tiles {m.sum():6d}  rows {int(rows[m].sum()):9d}  CTA-ms {ms[m].sum():8.1f}  max {ms[m].max() if m.any() else 0:7.2f} ms")
+srt = np.sort(ms)[::-1]
+for fr in (0.001, 0.01, 0.1):
+    k = max(1, int(len(srt) * fr))
+    print(f"  top {fr*100:.1f}% tiles: {srt[:k].sum():8.1f} CTA-ms of {ms.sum():.1f}")
+print(f"  ideal wall at 592 CTA slots: {ms.sum()/592:.1f} ms")
