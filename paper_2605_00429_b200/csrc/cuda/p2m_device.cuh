@@ -106,7 +106,9 @@ struct Params {
     double dmin[3], dmax[3];
     double prune_eps;
     double key_lo[3], key_scale[3];  // Morton key box
-    float f32_delta;        // additive slack of the conservative fp32 sphere pre-filter
+    float mesh_m;           // max |coordinate| of the mesh and of every stored centre / point (fp32 error scale)
+    float eps2;             // 2 * prune_eps, rounded up
+    float ctr_slack;        // max over faces of d(fp32 disk centre, face): |q - c| + this bounds d(q, face) from above
     const uint8_t* heavy;   // per site: 1 if its rows are tiled long_tile rows per CTA
     uint32_t long_tile;     // (32, 64, 128 or 256)
     // exact grid cell-locate (optional, grid_off == nullptr -> k-d tree only): every site whose
@@ -120,6 +122,7 @@ struct Params {
     int nns;                // P2M_NNS_* strategy of nearest_site
     int tile_order;         // scan launch order: 0 site order, 1 longest-first, 2 list-length buckets
     uint32_t small_chunks;  // tiles of <= 32 rows and lists of <= this many chunks: one warp per tile (0: off)
+    int warp_tiles;         // 1: every tile has <= 32 rows and is scanned by one warp (k_scan_small); no k_scan_tiles
     unsigned long long* tile_trace;  // debug (P2M_TILE_TRACE): per tile {site, rows, list length, cycles | sm}
     const uint64_t* adj_off;  // Delaunay adjacency CSR (nullptr: no DelaunayWalk)
     const uint32_t* adj;

@@ -87,8 +87,8 @@ float round_up_f(double v) {
 // n and two in-plane directions).  With nn = n / |n| in exact arithmetic, every point satisfies
 // |nn.(x - c)| <= t and |x - c|^2 - (nn.(x - c))^2 <= R^2.  Stored {c, 4 R^2} and {n, t + tslack},
 // both rounded up and inflated by 1e-12 (relative, and of the points' extent from c) over the fp64
-// evaluation here; tslack = the device's fp32 error of |h|.
-void fit_cyl(const double* x, int m, const double* nsum, const double* cen, double tslack, float4* out) {
+// evaluation here (the device adds its fp32 error of |h| per row).
+void fit_cyl(const double* x, int m, const double* nsum, const double* cen, float4* out) {
     double n[3] = {nsum[0], nsum[1], nsum[2]};
     double l = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
     if (!(l > 0.0) || !std::isfinite(l)) { n[0] = 0.0; n[1] = 0.0; n[2] = 1.0; l = 1.0; }
@@ -126,7 +126,7 @@ void fit_cyl(const double* x, int m, const double* nsum, const double* cen, doub
         r2 = std::max(r2, d2 - h * h);
         d2m = std::max(d2m, d2);
     }
-    t = t * (1.0 + 1e-12) + 1e-12 * std::sqrt(d2m) + tslack;
+    t = t * (1.0 + 1e-12) + 1e-12 * std::sqrt(d2m);
     r2 = r2 * (1.0 + 1e-12) + 1e-12 * d2m;
     out[0] = make_float4(cf[0], cf[1], cf[2], round_up_f(4.0 * r2));
     out[1] = make_float4(nf[0], nf[1], nf[2], round_up_f(t));
@@ -906,6 +906,8 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
         s->params.small_chunks = 2;  // measured on c2 (1, 2 > 4) and c5 (2 ~ 4 > 0)
         if (const char* v = std::getenv("P2M_SMALL_CHUNKS")) s->params.small_chunks = (uint32_t)std::min(4, std::max(0, std::atoi(v)));
         if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
+        s->params.warp_tiles = 0;
+        if (const char* v = std::getenv("P2M_SCAN_WARP")) s->params.warp_tiles = std::atoi(v) ? 1 : 0;
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
         s->params.adj = s->adj;
     }
@@ -997,7 +999,6 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     // device's fp32 error terms.
     double Mdom = 0.0;
     for (int c = 0; c < 3; ++c) Mdom = std::max({Mdom, std::fabs(d->domain_min[c]), std::fabs(d->domain_max[c])});
-    const double tslack = 40.0 * std::ldexp(1.0, -24) * Mdom;
     std::vector<float4> fcy(kCy * F);
     auto group_normal = [&](const uint32_t* ids, uint64_t k, double* nsum, std::vector<double>& pts) {
         nsum[0] = nsum[1] = nsum[2] = 0.0;
@@ -1016,9 +1017,26 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
         for (uint64_t f = f0; f < f1; ++f) {
             const uint32_t id = (uint32_t)f;
             group_normal(&id, 1, ns, pts);
-            fit_cyl(pts.data(), 3, ns, d->face_sphere + 4 * f, tslack, fcy.data() + kCy * f);
+            fit_cyl(pts.data(), 3, ns, d->face_sphere + 4 * f, fcy.data() + kCy * f);
         }
     });
+    // The disk centre is the face's min-enclosing-circle centre (the circumcentre of an acute face, the
+    // midpoint of the longest edge otherwise): a point of the face up to rounding.  The largest distance
+    // from a stored fp32 centre to its face makes |q - c| an upper bound of d(q, face) (scan d_min).
+    double ctr_slack = 0.0;
+    {
+        std::vector<double> part(F ? F : 1, 0.0);
+        parallel_sites(F, [&](uint64_t f0, uint64_t f1) {
+            for (uint64_t f = f0; f < f1; ++f) {
+                const double* t = d->tri_xyz + 9 * f;
+                const float4 c = fcy[kCy * f];
+                p2m::V3 cp;
+                part[f] = std::sqrt(p2m::closest_tri(p2m::V3{c.x, c.y, c.z}, p2m::ld3(t), p2m::ld3(t + 3), p2m::ld3(t + 6), &cp));
+            }
+        });
+        for (double v : part) ctr_slack = std::max(ctr_slack, v);
+        ctr_slack = ctr_slack * (1.0 + 1e-9) + 1e-12 * Mdom;
+    }
     // Spatial list order for the grouped scan (lfs): the (d^2, face id) argmin does not depend on
     // the order a list is scanned in, so each list is re-sorted by the Morton code of its faces'
     // sphere centres (ties by id) -- its 32-entry batches and 256-entry chunks then enclose compact
@@ -1102,13 +1120,13 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
                 const uint64_t je = std::min(b1, j + 32);
                 bpt[bi] = group_point(j, je);
                 group_normal(lfs.data() + j, je - j, ns, pts);
-                fit_cyl(pts.data(), (int)(3 * (je - j)), ns, nullptr, tslack, bcy.data() + kCy * bi);
+                fit_cyl(pts.data(), (int)(3 * (je - j)), ns, nullptr, bcy.data() + kCy * bi);
             }
             for (uint64_t j = b0, ci = coff[s]; j < b1; j += kListChunk, ++ci) {
                 const uint64_t je = std::min(b1, j + kListChunk);
                 cpt[ci] = group_point(j, je);
                 group_normal(lfs.data() + j, je - j, ns, pts);
-                fit_cyl(pts.data(), (int)(3 * (je - j)), ns, nullptr, tslack, ccy.data() + kCy * ci);
+                fit_cyl(pts.data(), (int)(3 * (je - j)), ns, nullptr, ccy.data() + kCy * ci);
             }
         }
     });
@@ -1127,14 +1145,17 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
     }
     P.prune_eps = 1e-9 * std::sqrt(dd2);  // same definition as the oracle (orc_ctx_create)
     {
-        // fp32 pre-filter slack: coordinates of every scanned query and sphere centre lie in D, so
-        // rounding each to fp32 moves |q - c| by at most 2*sqrt(3)*2^-24*M; doubled, plus 2 eps
-        double M = 0.0;
-        for (int c = 0; c < 3; ++c) M = std::max({M, std::fabs(d->domain_min[c]), std::fabs(d->domain_max[c])});
-        const double delta = 4.0 * std::sqrt(3.0) * std::ldexp(1.0, -24) * M + 2.0 * P.prune_eps;
-        float df = (float)delta;
-        if ((double)df < delta) df = std::nextafter(df, INFINITY);
-        P.f32_delta = df;
+        // fp32 error scale of the scan's bounds: the largest |coordinate| of the mesh and of every
+        // stored centre / point; the kernels take max(|q|, mesh_m) per row
+        float mm = 0.f;
+        for (uint64_t i = 0; i < 3 * F; ++i) mm = std::max(mm, round_up_f(std::fabs(d->tri_xyz[i])));
+        auto scan4 = [&](const std::vector<float4>& v, int stride) {
+            for (size_t i = 0; i < v.size(); i += stride) mm = std::max({mm, std::fabs(v[i].x), std::fabs(v[i].y), std::fabs(v[i].z)});
+        };
+        scan4(fcy, kCy); scan4(bcy, kCy); scan4(ccy, kCy); scan4(bpt, 1); scan4(cpt, 1);
+        P.mesh_m = mm;
+        P.eps2 = round_up_f(2.0 * P.prune_eps);
+        P.ctr_slack = round_up_f(ctr_slack);
     }
     P.long_tile = 32;
     if (const char* v = std::getenv("P2M_LONG_TILE")) {
@@ -1247,7 +1268,7 @@ struct Reader {
 template <class IO, class F>
 void params_fields(Params& P, F&& f) {
     for (int c = 0; c < 3; ++c) { f(P.dmin[c]); f(P.dmax[c]); f(P.key_lo[c]); f(P.key_scale[c]); f(P.grid_lo[c]); f(P.grid_inv[c]); f(P.grid_res[c]); }
-    f(P.prune_eps); f(P.f32_delta); f(P.long_tile); f(P.no_seed); f(P.no_batch); f(P.n_nodes); f(P.n_faces);
+    f(P.prune_eps); f(P.mesh_m); f(P.eps2); f(P.ctr_slack); f(P.long_tile); f(P.no_seed); f(P.no_batch); f(P.n_nodes); f(P.n_faces);
 }
 
 template <class T>

@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(256) k_tile_flags(Params p, const uint32_t* __
     const uint32_t rs = run_start[i];
     uint32_t T = kTile;
     if (k < n_sites && p.heavy[k]) T = p.long_tile;
+    if (p.warp_tiles) T = 32;
     flag[i] = (k < n_sites && ((uint32_t)i == rs || (((uint32_t)i - rs) % T) == 0)) ? 1u : 0u;
     // number of table rows (fallback rows sort last)
     const bool last_valid = k < n_sites && (i + 1 == n || key[i + 1] >= n_sites);
@@ -208,6 +209,23 @@ __device__ __forceinline__ uint64_t fma2_dn(uint64_t a, uint64_t b, uint64_t c) 
 // For one face (t ~ 0, R = its min-enclosing radius) this is the distance to its bounding disk: on
 // c5, 5 faces per query pass it against 334 for the bounding sphere (same final d_min).
 constexpr float kRhoErr = 24.0f / 16777216.0f;   // 24 * 2^-24
+// Per-row fp32 error scale Mq = max(|q_f|_inf, mesh_m) (every centre, point and mesh coordinate is
+// within mesh_m): |q - q_f| <= sqrt(3) u Mq, an fp32 point P of the mesh is within sqrt(3) u Mq of
+// the exact one, and the cylinder test's |h| is within 21 u Mq of exact.
+constexpr float kUbSlack = 6.929e-7f;   // >= 2 * 2 sqrt(3) * 2^-24: rounding of q and of P in |q_f - P_f|
+constexpr float kDkSlack = 2.8e-6f;     // >= (4 sqrt(3) + 40) * 2^-24: q rounding in the prunes + |h| error
+__device__ __forceinline__ float row_scale(const Params& p, float qx, float qy, float qz) {
+    return fmaxf(fmaxf(fabsf(qx), fabsf(qy)), fmaxf(fabsf(qz), p.mesh_m));
+}
+// the row's pruning bound DK from a rigorous upper bound ub of its distance to the mesh:
+// (ub + slack(Mq) + 2 eps) * (1 + 1e-6), rounded up
+__device__ __forceinline__ float dk_of(const Params& p, float ub, float Mq) {
+    return __fmul_ru(__fadd_ru(ub, __fmaf_ru(Mq, kDkSlack, p.eps2)), 1.000001f);
+}
+// upper bound of |q - P| from the fp32 d2f = |q_f - P_f|^2 (P on the mesh)
+__device__ __forceinline__ float ub_of(float d2f, float Mq) {
+    return __fadd_ru(__fmul_ru(__fsqrt_ru(d2f), 1.000001f), __fmul_ru(Mq, kUbSlack));
+}
 
 // may some point of the cylinder lie within U of q_f (U2 = U^2 rounded up)?  false = prune
 __device__ __forceinline__ bool cyl_near(float qx, float qy, float qz, float U2, float4 c0, float4 c1) {
@@ -254,6 +272,7 @@ constexpr int kWarps = kTile / 32;
 // operands: pair pp = candidates (2pp, 2pp+1) occupies 16 floats
 //   (cx0,cx1,cy0,cy1) (cz0,cz1,R4_0,R4_1) (nx0,nx1,ny0,ny1) (nz0,nz1,t0,t1)
 // stage_disk writes candidate k's record (r0 = {c, 4R^2}, r1 = {n, t}) into that layout.
+#define kPadDisk make_float4(1e18f, 1e18f, 1e18f, 0.f)  // record of a padding entry: far away, never passes
 __device__ __forceinline__ void stage_disk(float* pf, int k, float4 r0, float4 r1) {
     float* b = pf + 16 * (k >> 1) + (k & 1);
     b[0] = r0.x; b[2] = r0.y; b[4] = r0.z; b[6] = r0.w;
@@ -274,9 +293,8 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
                                                unsigned long long& rare_iters, unsigned long long& sbytes,
                                                const float4* disk, const uint32_t* fid, int valid, int lane,
                                                float* sdk) {
-    const float K = 1.000001f;
-    const float delta = p.f32_delta;
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
+    const float Mq = row_scale(p, qxf, qyf, qzf);
     uint32_t mask = 0;
     if (active && sdk) {                         // the row's bound as tightened by the other replicas
         float dkx, dky;
@@ -290,6 +308,7 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         const float u2 = __fmul_ru(dkx, dkx);
         const uint64_t U2 = pk2(u2, u2);
         const uint64_t NRHO = pk2(-kRhoErr, -kRhoErr), M4 = pk2(-4.f, -4.f), Q = pk2(0.25f, 0.25f);
+        float smin = __int_as_float(0x7f800000);  // min |q_f - c|^2 over the batch's disk centres
 #pragma unroll 4
         for (int pp = 0; pp < 16; ++pp) {
             const float4 A0 = disk[4 * pp], A1 = disk[4 * pp + 1], A2 = disk[4 * pp + 2], A3 = disk[4 * pp + 3];
@@ -299,6 +318,11 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
             const uint64_t h = fma2(vz, pk2(A3.x, A3.y), fma2(vy, pk2(A2.z, A2.w), mul2(vx, pk2(A2.x, A2.y))));
             const uint64_t S = fma2(vz, vz, fma2(vy, vy, mul2(vx, vx)));
             const uint64_t rl = fma2(S, NRHO, sub2(S, mul2(h, h)));        // <= rho^2
+            {
+                float s0, s1;
+                upk2(S, s0, s1);
+                smin = fminf(smin, fminf(s0, s1));
+            }
             float h0, h1;
             upk2(h, h0, h1);
             const float a0 = fmaxf(fabsf(h0) - A3.z, 0.f), a1 = fmaxf(fabsf(h1) - A3.w, 0.f);
@@ -323,6 +347,16 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         }
         mask = ~__brev(mask);  // bit k = candidate k passes
         if (valid < 32) mask &= (1u << valid) - 1u;
+        // every disk centre is a point of its face (up to ctr_slack): |q - c| bounds the row's distance
+        // from above, so the nearest staged centre tightens d_min before the exact tests (padding
+        // entries sit at 1e18, kPadDisk, and never count)
+        if (!p.no_seed) {
+            const float dkf = dk_of(p, __fadd_ru(ub_of(smin, Mq), p.ctr_slack), Mq);
+            if (dkf < dkx) {
+                DK = pk2(dkf, dkf);
+                if (sdk) atomicMin(reinterpret_cast<int*>(sdk), __float_as_int(dkf));
+            }
+        }
     }
     uint32_t um = __reduce_or_sync(0xffffffffu, mask);
     if (kCounters) {
@@ -349,7 +383,7 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
             bf = f;
             // any upper bound of sqrt(best) is a valid d_min for the prunes: the fp32 sqrt rounded up of
             // best rounded up (cheaper than the fp64 sqrt)
-            const float dkf = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(dd)), delta), K);
+            const float dkf = dk_of(p, __fsqrt_ru(__double2float_ru(dd)), Mq);
             float dkx, dky;
             upk2(DK, dkx, dky);
             if (dkf < dkx) {
@@ -374,10 +408,9 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
 template <bool kCounters>
 __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q, uint64_t QX, uint64_t QY,
                                          uint64_t QZ, double& dmin, uint64_t& DK) {
-    const float K = 1.000001f;
-    const float delta = p.f32_delta;
     const float finf = __int_as_float(0x7f800000);
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
+    const float Mq = row_scale(p, qxf, qyf, qzf);
     const uint64_t bo = p.boff[s], co = p.coff[s];
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
     if (!p.no_seed) {
@@ -389,7 +422,7 @@ __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q
         const D4 rf = ldg4(p.site_ref + s);
         if (rf.w != 0.0) {
             dmin = sqrt(vd2(q, V{rf.x, rf.y, rf.z}));
-            const float dkf = __fmul_ru(__fadd_ru(__double2float_ru(dmin), delta), K);
+            const float dkf = dk_of(p, __double2float_ru(dmin), Mq);
             DK = pk2(dkf, dkf);
         }
     }
@@ -405,7 +438,7 @@ __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q
             const float4 c = p.cpt[co + c2];  // same address across the tile's lanes: broadcast
             const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
             const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            const float u = __fmul_ru(__fsqrt_ru(d2f), 1.000001f);
+            const float u = ub_of(d2f, Mq);
             if (u < ub) { ub = u; bc = c2; }
         }
         const uint64_t nbl = p.boff[s + 1] - bo;
@@ -414,26 +447,25 @@ __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q
             const float4 c = p.bpt[bo + b2];
             const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
             const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            ub = fminf(ub, __fmul_ru(__fsqrt_ru(d2f), 1.000001f));
+            ub = fminf(ub, ub_of(d2f, Mq));
         }
-        ub = __fadd_ru(ub, delta);
         if ((double)ub < dmin) {
             dmin = (double)ub;
-            const float dkf = __fmul_ru(__fadd_ru(ub, delta), K);
+            const float dkf = dk_of(p, ub, Mq);
             DK = pk2(dkf, dkf);
         }
     }
 }
 
-// ---- small tiles: one warp per tile ----------------------------------------------------------
-// A tile of at most 32 rows whose list has at most kSmallChunks chunks is scanned by ONE warp (lanes
-// = rows) instead of a whole CTA, so a CTA works on 8 such tiles at once.  It runs on a side stream
-// concurrently with k_scan_tiles (whose CTAs skip these tiles), so neither waits for the other's tail.  Most of a small tile's
-// time is the latency of its dependent gathers (seeds, list entries, records), which the 8x more
-// tiles in flight per SM hide; the per-row semantics -- seeds, chunk and batch sphere prunes,
-// best-first visiting for the tile's first row, the batch scan -- are those of k_scan_tiles.
-constexpr uint32_t kSmallChunks = 4;
-
+// ---- warp tiles: one warp per tile of <= 32 rows --------------------------------------------
+// A tile of at most 32 rows is scanned by ONE warp (lanes = rows), 8 independent tiles per CTA, with
+// no block barrier: the warp walks its site's list on its own.  Chunks are taken in windows of 32
+// (lane k holds chunk k's cylinder): a level-0 vote keeps the chunks some row may need, ranked by
+// the lower bound of the tile's first row (best-first); each kept chunk is re-tested with the current
+// d_min, its batch cylinders are voted on (level 1) in the same best-first order, and each needed
+// batch is staged in the warp's shared-memory slice and scanned (level 2 + exact, scan_batch_row).
+// Used for the small tiles beside k_scan_tiles (side stream), and for every tile in warp mode
+// (Params::warp_tiles: 32-row tiles everywhere, k_scan_tiles not launched).
 #ifndef P2M_SMALL_MINB
 #define P2M_SMALL_MINB 4
 #endif
@@ -458,6 +490,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     const int m = (int)(stop - start);
     const uint32_t s = key[start];
     const bool active = lane < m;
+    const long long t_start = p.tile_trace ? clock64() : 0;
     const float finf = __int_as_float(0x7f800000);
     uint32_t row = 0;
     V q{0, 0, 0};
@@ -479,72 +512,92 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     const uint64_t bo = p.boff[s], co = p.coff[s];
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
-    if (kCounters && lane == 0) sbytes += 48ull * nch + 76;  // chunk spheres + cylinders, site ref, offsets, tile meta
+    if (kCounters && lane == 0) sbytes += 16ull * nch + 76;  // chunk points, site ref, offsets, tile meta
     // conservative "may some member be within d_min" test of this lane's row against a group cylinder
     auto near = [&](float4 c0, float4 c1) {
         float dkx, dky;
         upk2(DK, dkx, dky);
         return cyl_near(fx, fy, fz, __fmul_ru(dkx, dkx), c0, c1);
     };
-    // chunks best-first (<= 4: every lane ranks them identically)
-    uint32_t ck[kSmallChunks], ci[kSmallChunks];
-#pragma unroll
-    for (uint32_t c = 0; c < kSmallChunks; ++c) {
-        ck[c] = c < nch ? (nch > 1 ? cyl_key(rx, ry, rz, p.ccy[kCy * (co + c)], p.ccy[kCy * (co + c) + 1]) : 0u) : 0xffffffffu;
-        ci[c] = c;
-    }
-#pragma unroll
-    for (int i = 1; i < (int)kSmallChunks; ++i)
-#pragma unroll
-        for (int j = i; j > 0; --j)
-            if (ck[j] < ck[j - 1]) {
-                const uint32_t tk = ck[j]; ck[j] = ck[j - 1]; ck[j - 1] = tk;
-                const uint32_t tc = ci[j]; ci[j] = ci[j - 1]; ci[j - 1] = tc;
-            }
-    float* wdf = reinterpret_cast<float*>(wd);
-    for (uint32_t oc = 0; oc < nch; ++oc) {
-        const uint32_t cidx = ci[oc];
-        if (nch > 1 && !p.no_batch &&
-            !__any_sync(0xffffffffu, active && near(p.ccy[kCy * (co + cidx)], p.ccy[kCy * (co + cidx) + 1])))
-            continue;
-        const uint64_t cb = beg + (uint64_t)cidx * kChunk;
-        const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
-        if (kCounters && lane == 0) sbytes += 32ull * nb;  // the chunk's batch cylinders
-        // the chunk's batches best-first for the first row
-        float4 b0c = make_float4(0.f, 0.f, 0.f, 0.f), b1c = b0c;
-        uint32_t bk = 0xffffffffu;
-        if (lane < nb) {
-            const uint64_t gi = kCy * (bo + (uint64_t)cidx * (kChunk / 32) + lane);
-            b0c = p.bcy[gi];
-            b1c = p.bcy[gi + 1];
-            bk = cyl_key(rx, ry, rz, b0c, b1c);
-        }
+    auto bcast = [&](float4 v, int src) {
+        return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                           __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+    };
+    // rank of this lane's key among the lanes whose key is not ~0 (ties by lane): best-first order
+    auto rank_of = [&](uint32_t k) {
         uint32_t rk = 0;
-#pragma unroll
-        for (int j = 0; j < kChunk / 32; ++j) {
-            const uint32_t kj = __shfl_sync(0xffffffffu, bk, j);
-            rk += (kj < bk || (kj == bk && j < lane)) ? 1u : 0u;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t kj = __shfl_sync(0xffffffffu, k, j);
+            rk += (kj < k || (kj == k && j < lane)) ? 1u : 0u;
         }
-        for (int pos = 0; pos < nb; ++pos) {
-            const int src = __ffs(__ballot_sync(0xffffffffu, lane < nb && rk == (uint32_t)pos)) - 1;
-            const float4 c0 = make_float4(__shfl_sync(0xffffffffu, b0c.x, src), __shfl_sync(0xffffffffu, b0c.y, src),
-                                          __shfl_sync(0xffffffffu, b0c.z, src), __shfl_sync(0xffffffffu, b0c.w, src));
-            const float4 c1 = make_float4(__shfl_sync(0xffffffffu, b1c.x, src), __shfl_sync(0xffffffffu, b1c.y, src),
-                                          __shfl_sync(0xffffffffu, b1c.z, src), __shfl_sync(0xffffffffu, b1c.w, src));
-            if (!p.no_batch && !__any_sync(0xffffffffu, active && near(c0, c1))) continue;  // pruned whole
-            const uint64_t b0 = cb + 32ull * src;
-            const int valid = (int)min((uint64_t)32, end - b0);
-            uint32_t f = 0;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-            if (lane < valid) { f = p.lfs[b0 + lane]; r0 = p.fcy[kCy * (uint64_t)f]; r1 = p.fcy[kCy * (uint64_t)f + 1]; }
-            wf[lane] = f;
-            stage_disk(wdf, lane, r0, r1);
-            __syncwarp();
-            if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
-            scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
-                                      wd, wf, valid, lane, nullptr);
-            __syncwarp();                        // the slice is rewritten by the next batch
+        return rk;
+    };
+    float* wdf = reinterpret_cast<float*>(wd);
+    for (uint32_t w0 = 0; w0 < nch; w0 += 32) {
+        const int wn = (int)min(32u, nch - w0);
+        float4 cc0 = make_float4(0.f, 0.f, 0.f, 0.f), cc1 = cc0;  // lane k: chunk w0 + k's cylinder
+        if (lane < wn) { cc0 = p.ccy[kCy * (co + w0 + lane)]; cc1 = p.ccy[kCy * (co + w0 + lane) + 1]; }
+        if (kCounters && lane == 0) sbytes += 32ull * wn;
+        // level 0: the chunks of the window some row may need
+        uint32_t cneed = 0;
+        if (nch == 1 || p.no_batch) {
+            cneed = wn == 32 ? 0xffffffffu : ((1u << wn) - 1u);
+        } else {
+            for (int k = 0; k < wn; ++k) {
+                const float4 c0 = bcast(cc0, k), c1 = bcast(cc1, k);
+                if (__any_sync(0xffffffffu, active && near(c0, c1))) cneed |= 1u << k;
+            }
         }
+        const int nn = __popc(cneed);
+        const uint32_t crk = rank_of(((cneed >> lane) & 1u) ? (nn > 1 ? cyl_key(rx, ry, rz, cc0, cc1) : 0u) : 0xffffffffu);
+        for (int pos = 0; pos < nn; ++pos) {
+            const int src = __ffs(__ballot_sync(0xffffffffu, ((cneed >> lane) & 1u) && crk == (uint32_t)pos)) - 1;
+            const uint32_t cidx = w0 + (uint32_t)src;
+            if (pos > 0 && !p.no_batch) {        // re-test with the d_min the earlier chunks produced
+                const float4 c0 = bcast(cc0, src), c1 = bcast(cc1, src);
+                if (!__any_sync(0xffffffffu, active && near(c0, c1))) continue;
+            }
+            const uint64_t cb = beg + (uint64_t)cidx * kChunk;
+            const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
+            if (kCounters && lane == 0) sbytes += 32ull * nb;  // the chunk's batch cylinders
+            // the chunk's batches best-first for the first row
+            float4 b0c = make_float4(0.f, 0.f, 0.f, 0.f), b1c = b0c;
+            uint32_t bk = 0xffffffffu;
+            if (lane < nb) {
+                const uint64_t gi = kCy * (bo + (uint64_t)cidx * (kChunk / 32) + lane);
+                b0c = p.bcy[gi];
+                b1c = p.bcy[gi + 1];
+                bk = nb > 1 ? cyl_key(rx, ry, rz, b0c, b1c) : 0u;
+            }
+            const uint32_t rk = rank_of(bk);
+            for (int bpos = 0; bpos < nb; ++bpos) {
+                const int bsrc = __ffs(__ballot_sync(0xffffffffu, lane < nb && rk == (uint32_t)bpos)) - 1;
+                if (!p.no_batch) {
+                    const float4 c0 = bcast(b0c, bsrc), c1 = bcast(b1c, bsrc);
+                    if (!__any_sync(0xffffffffu, active && near(c0, c1))) continue;  // pruned whole
+                }
+                const uint64_t b0 = cb + 32ull * bsrc;
+                const int valid = (int)min((uint64_t)32, end - b0);
+                uint32_t f = 0;
+                float4 r0 = kPadDisk, r1 = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (lane < valid) { f = p.lfs[b0 + lane]; r0 = p.fcy[kCy * (uint64_t)f]; r1 = p.fcy[kCy * (uint64_t)f + 1]; }
+                wf[lane] = f;
+                stage_disk(wdf, lane, r0, r1);
+                __syncwarp();
+                if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
+                scan_batch_row<kCounters>(p, active, q, QX, QY, QZ, DK, best, bf, exact, passes, rare_iters, sbytes,
+                                          wd, wf, valid, lane, nullptr);
+                __syncwarp();                    // the slice is rewritten by the next batch
+            }
+        }
+    }
+    if (p.tile_trace && lane == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* t = p.tile_trace + 4 * (uint64_t)b;
+        t[0] = s; t[1] = (unsigned long long)m; t[2] = end - beg;
+        t[3] = (unsigned long long)(clock64() - t_start) << 8 | (smid & 0xff);
     }
     if (active) {
         V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
@@ -645,7 +698,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
     }
     const float finf = __int_as_float(0x7f800000);
     double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
-    uint64_t DK = pk2(finf, finf);               // (dmin_up + delta) * K, rounded up, both halves
+    uint64_t DK = pk2(finf, finf);               // dk_of(upper bound of the row's distance), both halves
     uint32_t bf = 0xffffffffu;
     uint32_t exact = 0;
     unsigned long long passes = 0, rare_iters = 0;  // diagnostics (counters mode only)
@@ -661,7 +714,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
 #define qzf __uint_as_float((uint32_t)QZ)
     // register prefetch of one chunk entry per thread: face id + its disk record
     uint32_t nf = 0;
-    float4 nv0 = make_float4(0.f, 0.f, 0.f, 0.f), nv1 = nv0;
+    float4 nv0 = kPadDisk, nv1 = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t pre_c = 0xffffffffu;                // chunk held in (nf, nv0, nv1)
     bool first_chunk = true;
 #if P2M_EARLY1
@@ -792,7 +845,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                 if (!__any_sync(0xffffffffu, need)) continue;  // pruned whole by its batch cylinder
                 if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
                 uint32_t f = 0;
-                float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+                float4 r0 = kPadDisk, r1 = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (lane < valid) { f = p.lfs[b0 + lane]; r0 = p.fcy[kCy * (uint64_t)f]; r1 = p.fcy[kCy * (uint64_t)f + 1]; }
                 wf[lane] = f;
                 stage_disk(wdf, lane, r0, r1);
@@ -811,8 +864,8 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
             first_chunk = false;
             if (pre_c != cidx) {
                 nf = 0;
-                nv0 = make_float4(0.f, 0.f, 0.f, 0.f);
-                nv1 = nv0;
+                nv0 = kPadDisk;
+                nv1 = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (tid < mc) { nf = p.lfs[base + tid]; nv0 = p.fcy[kCy * (uint64_t)nf]; nv1 = p.fcy[kCy * (uint64_t)nf + 1]; }
             }
             // level 1: the enclosing cylinder of each 32-entry batch.  If every lane's conservative
@@ -853,8 +906,8 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
                     const uint32_t c2 = w0 + (nch > 1 ? s_oidx[oi + 1] : 0u);
                     const uint64_t b2 = beg + (uint64_t)c2 * kChunk;
                     nf = 0;
-                    nv0 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    nv1 = nv0;
+                    nv0 = kPadDisk;
+                    nv1 = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (b2 + tid < end) { nf = p.lfs[b2 + tid]; nv0 = p.fcy[kCy * (uint64_t)nf]; nv1 = p.fcy[kCy * (uint64_t)nf + 1]; }
                     pre_c = c2;
                 }
@@ -1068,8 +1121,8 @@ __global__ void __launch_bounds__(256) k_tile_keys(Params p, const uint32_t* __r
         const uint32_t s = key[start];
         const uint64_t len0 = p.off[s + 1] - p.off[s];
         const uint64_t len = len0 < (1u << 20) ? len0 : (1u << 20);
-        small = stop - start <= 32u && p.coff[s + 1] - p.coff[s] <= p.small_chunks;
-        if (small) k = 1u;                       // after every CTA tile: k_scan_small's range
+        small = p.warp_tiles || (stop - start <= 32u && p.coff[s + 1] - p.coff[s] <= p.small_chunks);
+        if (small && !p.warp_tiles) k = 1u;      // after every CTA tile: k_scan_small's range
         else if (p.tile_order == 1) k = (uint32_t)((len * (uint64_t)(stop - start + 16)) >> 4) + 2u;
         else if (p.tile_order == 2) k = (uint32_t)(64 - __clzll((long long)len)) + 2u;  // coarse buckets
         else k = 2u;                             // site order (the sort is stable)
@@ -1109,6 +1162,12 @@ cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* 
     if (!order) return cudaErrorInvalidValue;   // the launch order (launch_tile_order) is required
     const unsigned g = (unsigned)max_tiles(n, p.n_nodes);
     cudaError_t e;
+    if (p.warp_tiles) {                          // warp mode: every tile is a warp tile
+        const unsigned gs = (g + kWarps - 1) / kWarps;
+        if (counters) k_scan_small<true><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_small<false><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+        return cudaGetLastError();
+    }
     const bool small = p.small_chunks && side;
     if (small) {                                 // fork: small tiles on the side stream
         if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;

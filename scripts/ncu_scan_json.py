@@ -41,8 +41,8 @@ for d in kern:
     last["tiles" if "k_scan_tiles" in d["Kernel Name"] else "small"] = d
 ks = list(last.values())
 unit = {h: rr[1][i] for i, h in enumerate(hdr)}
-tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}[unit.get("gpu__time_duration.sum", "nsecond")]
-bscale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}[unit.get("gpu__time_duration.sum", "nsecond")]
+bscale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9, "TB": 1e12}
 
 
 def b(d, k):
