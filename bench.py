@@ -500,9 +500,9 @@ def main():
     # Roofline of the dominant kernel (the scan phase: k_scan_tiles || k_scan_small).  Algorithmic
     # bytes per launch = 64 B per row (q + row index in, distance + closest point + face out) + the
     # structure bytes the scan kernels load, counted by the kernels themselves in the counters pass:
-    # each staged list chunk (face ids, fp32 sphere and lower-bound records, group spheres) ONCE per
-    # tile, each face record once per warp visit -- never per row.  Over the scan's mean time measured
-    # with CUDA events on the query stream in the timed region.
+    # each staged batch (face ids + face disks) once per tile or warp tile, group records once per
+    # visit, each face record once per exact test -- never per row.  Over the scan's mean time
+    # measured with CUDA events on the query stream in the timed region.
     t_scan_s = split[4] / 1e3 if split[4] > 0 else ms / 1e3
     B_scan = ROW_BYTES * n + c["structure_bytes"]
     achieved = B_scan / t_scan_s / 1e9
@@ -542,10 +542,11 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "scan phase: k_scan_tiles || k_scan_small (site-tiled pruned list scan, exact fp64)",
                      "algorithmic_bytes_per_launch": B_scan,
-                     "bytes_model": "64 B/row (q, row index, distance, closest point, face) + structure bytes loaded "
-                                    "by the scan kernels (staged chunk = 20 B/entry ids+fp32 spheres + 96 B/entry "
-                                    "lower-bound records of needed batches + 16 B/group sphere, once per tile; "
-                                    "96 B face record per warp visit) -- counted in-kernel",
+                     "bytes_model": "64 B/row (q, row index, distance, closest point, face) + the structure bytes the "
+                                    "scan kernels load, counted in-kernel: per tile the list's chunk points and "
+                                    "cylinders (16 + 32 B per chunk) and 76 B of offsets/meta; per visited chunk its "
+                                    "batch cylinders (32 B each); per staged batch 36 B/entry (face id + face disk); "
+                                    "96 B face record per exact test",
                      "measured_dram_gbs": (traffic / t_scan_s / 1e9) if traffic else None,
                      "compute": compute,
                      "peak_source": peak_src},

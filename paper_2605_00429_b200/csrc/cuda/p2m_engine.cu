@@ -660,6 +660,10 @@ int run_pipeline(p2m_engine* E, Slot& s, const double* d_q, uint64_t n, const p2
         std::lock_guard<std::mutex> lk(s.pmu);
         sp = s.params;  // one consistent snapshot per call
     }
+    // warp tiles for the sites that are not heavy when rows are sparse per site (measured: c5, 51 rows
+    // per site, +2%, c1 +13%; dense batches -- c2, 570 rows per site -- keep the CTA tiles, whose
+    // staged chunks serve up to 256 rows); P2M_WARP_MIN_CHUNKS overrides (0 = off)
+    if (sp.warp_min_chunks == ~0u) sp.warp_min_chunks = (n < 128ull * E->n_sites) ? 1u : 0u;
     int order = sp.tile_order;
     if (order < 0) order = n < (4ull << 20) ? 1 : 0;
     const bool lpt = true;  // the launch order array (site order, LPT or buckets; small tiles last) always exists
@@ -908,6 +912,8 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
         if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
         s->params.warp_tiles = 0;
         if (const char* v = std::getenv("P2M_SCAN_WARP")) s->params.warp_tiles = std::atoi(v) ? 1 : 0;
+        s->params.warp_min_chunks = ~0u;  // auto (run_pipeline)
+        if (const char* v = std::getenv("P2M_WARP_MIN_CHUNKS")) s->params.warp_min_chunks = (uint32_t)std::max(0, std::atoi(v));
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
         s->params.adj = s->adj;
     }

@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(256) k_tile_flags(Params p, const uint32_t* __
     const uint32_t k = key[i];
     const uint32_t rs = run_start[i];
     uint32_t T = kTile;
-    if (k < n_sites && p.heavy[k]) T = p.long_tile;
+    if (k < n_sites) {
+        if (p.heavy[k]) T = p.long_tile;
+        else if (p.warp_min_chunks && p.coff[k + 1] - p.coff[k] >= p.warp_min_chunks) T = 32;  // warp tiles
+    }
     if (p.warp_tiles) T = 32;
     flag[i] = (k < n_sites && ((uint32_t)i == rs || (((uint32_t)i - rs) % T) == 0)) ? 1u : 0u;
     // number of table rows (fallback rows sort last)
@@ -523,15 +526,13 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
         return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
                            __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
     };
-    // rank of this lane's key among the lanes whose key is not ~0 (ties by lane): best-first order
-    auto rank_of = [&](uint32_t k) {
-        uint32_t rk = 0;
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) {
-            const uint32_t kj = __shfl_sync(0xffffffffu, k, j);
-            rk += (kj < k || (kj == k && j < lane)) ? 1u : 0u;
-        }
-        return rk;
+    // best-first order without sorting: take the lane holding the smallest key (ties: the lowest
+    // lane) and retire it; keys of the items to visit are < ~0 (non-negative float bits)
+    auto take_min = [&](uint32_t& k) {
+        const uint32_t mk = __reduce_min_sync(0xffffffffu, k);
+        const int src = __ffs(__ballot_sync(0xffffffffu, k == mk)) - 1;
+        if (lane == src) k = 0xffffffffu;
+        return src;
     };
     float* wdf = reinterpret_cast<float*>(wd);
     for (uint32_t w0 = 0; w0 < nch; w0 += 32) {
@@ -550,9 +551,9 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
             }
         }
         const int nn = __popc(cneed);
-        const uint32_t crk = rank_of(((cneed >> lane) & 1u) ? (nn > 1 ? cyl_key(rx, ry, rz, cc0, cc1) : 0u) : 0xffffffffu);
+        uint32_t ckey = ((cneed >> lane) & 1u) ? (nn > 1 ? cyl_key(rx, ry, rz, cc0, cc1) : 0u) : 0xffffffffu;
         for (int pos = 0; pos < nn; ++pos) {
-            const int src = __ffs(__ballot_sync(0xffffffffu, ((cneed >> lane) & 1u) && crk == (uint32_t)pos)) - 1;
+            const int src = take_min(ckey);
             const uint32_t cidx = w0 + (uint32_t)src;
             if (pos > 0 && !p.no_batch) {        // re-test with the d_min the earlier chunks produced
                 const float4 c0 = bcast(cc0, src), c1 = bcast(cc1, src);
@@ -570,9 +571,8 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
                 b1c = p.bcy[gi + 1];
                 bk = nb > 1 ? cyl_key(rx, ry, rz, b0c, b1c) : 0u;
             }
-            const uint32_t rk = rank_of(bk);
             for (int bpos = 0; bpos < nb; ++bpos) {
-                const int bsrc = __ffs(__ballot_sync(0xffffffffu, lane < nb && rk == (uint32_t)bpos)) - 1;
+                const int bsrc = take_min(bk);
                 if (!p.no_batch) {
                     const float4 c0 = bcast(b0c, bsrc), c1 = bcast(b1c, bsrc);
                     if (!__any_sync(0xffffffffu, active && near(c0, c1))) continue;  // pruned whole
@@ -1121,7 +1121,9 @@ __global__ void __launch_bounds__(256) k_tile_keys(Params p, const uint32_t* __r
         const uint32_t s = key[start];
         const uint64_t len0 = p.off[s + 1] - p.off[s];
         const uint64_t len = len0 < (1u << 20) ? len0 : (1u << 20);
-        small = p.warp_tiles || (stop - start <= 32u && p.coff[s + 1] - p.coff[s] <= p.small_chunks);
+        const uint64_t nch = p.coff[s + 1] - p.coff[s];
+        small = p.warp_tiles || (stop - start <= 32u && (nch <= p.small_chunks ||
+                                 (p.warp_min_chunks && nch >= p.warp_min_chunks && !p.heavy[s])));
         if (small && !p.warp_tiles) k = 1u;      // after every CTA tile: k_scan_small's range
         else if (p.tile_order == 1) k = (uint32_t)((len * (uint64_t)(stop - start + 16)) >> 4) + 2u;
         else if (p.tile_order == 2) k = (uint32_t)(64 - __clzll((long long)len)) + 2u;  // coarse buckets
@@ -1168,20 +1170,27 @@ cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* 
         else k_scan_small<false><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
         return cudaGetLastError();
     }
-    const bool small = p.small_chunks && side;
-    if (small) {                                 // fork: small tiles on the side stream
-        if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
+    // warp tiles (small lists, or every non-heavy site in sparse batches): k_scan_small, on a side
+    // stream forked from and joined back to s when there is one, so it overlaps k_scan_tiles
+    const bool small = p.small_chunks || p.warp_min_chunks;
+    const bool fork_side = small && side;
+    if (small) {
+        cudaStream_t ss = s;
+        if (fork_side) {
+            if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
+            ss = side;
+        }
         const unsigned gs = (g + kWarps - 1) / kWarps;
-        if (counters) k_scan_small<true><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
-        else k_scan_small<false><<<gs, kTile, 0, side>>>(p, q, rows, key, tiles, meta, order, o);
+        if (counters) k_scan_small<true><<<gs, kTile, 0, ss>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_small<false><<<gs, kTile, 0, ss>>>(p, q, rows, key, tiles, meta, order, o);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(join, side)) != cudaSuccess) return e;
+        if (fork_side && (e = cudaEventRecord(join, side)) != cudaSuccess) return e;
     }
     if (counters) k_scan_tiles<true><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
     else k_scan_tiles<false><<<g, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (small && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;  // join
+    if (fork_side && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;  // join
     return cudaGetLastError();
 }
 

@@ -49,15 +49,35 @@ def b(d, k):
     return f(d, k) * bscale.get(unit.get(k, "byte"), 1)
 
 
+try:
+    PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    PEAK = 6650.0
 t = [f(d, "gpu__time_duration.sum") * tscale for d in ks]
-T = sum(t)
-w = lambda k: sum(f(d, k) * ti for d, ti in zip(ks, t)) / T  # noqa: E731  duration-weighted
-dram = sum(b(d, "dram__bytes_read.sum") + b(d, "dram__bytes_write.sum") for d in ks)
+T = sum(x for x in t if x == x)
+
+
+def w(k):
+    # duration-weighted over the kernels that report the metric (a launch with no work has none)
+    num = den = 0.0
+    for d, ti in zip(ks, t):
+        v = f(d, k)
+        if v == v and ti == ti:
+            num += v * ti
+            den += ti
+    return num / den if den else float("nan")
+
+
+def nz(x):
+    return x if x == x else 0.0
+
+
+dram = sum(nz(b(d, "dram__bytes_read.sum")) + nz(b(d, "dram__bytes_write.sum")) for d in ks)
 res = {
     "config": cfg, "rows": rows, "kernels": [d["Kernel Name"][:60] for d in ks],
     "lib_sha256": hashlib.sha256(open(lib, "rb").read()).hexdigest(),
     "gpu_time_s": T, "dram_bytes_per_launch": dram, "dram_gbs_under_ncu": dram / T / 1e9,
-    "dram_pct": w("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+    "dram_pct": 100.0 * dram / T / 1e9 / PEAK,
     "l2_hit_pct": w("lts__t_sector_hit_rate.pct"),
     "fp64_pipe_pct": w("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
     "fma_pipe_pct": w("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),

@@ -321,6 +321,10 @@ def test_host_api_chunk_schedules_identical(c2, chunks, monkeypatch):
     {"P2M_HEAVY_E": "16"},                     # many more heavy sites (short tiles)
     {"P2M_NO_SEED": "1"}, {"P2M_NO_BATCH": "1"},  # without the d_min seeds / group-sphere levels
     {"P2M_NO_SPATIAL": "1"},                   # lists scanned in ascending face order
+    {"P2M_SCAN_WARP": "1"},                    # every tile a 32-row warp tile (no CTA tiles)
+    {"P2M_WARP_MIN_CHUNKS": "0"},              # no warp tiles beyond the small-list ones
+    {"P2M_WARP_MIN_CHUNKS": "3"},              # warp tiles only for lists of >= 3 chunks
+    {"P2M_SMALL_CHUNKS": "0", "P2M_WARP_MIN_CHUNKS": "1"},  # warp tiles without small-list tiles
 ])
 def test_scan_schedules_identical(c2, env, monkeypatch):
     """The tile partition (CTA tiles vs one-warp small tiles), their launch order, the Morton
