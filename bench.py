@@ -246,27 +246,34 @@ def parity_rows(ref, gpu, n):
     return int(ok.sum())
 
 
-def lib_sha256(path):
+def src_sha256():
+    """Hash of the CUDA sources, the ABI header and the build flags: identifies the build the ncu
+    evidence was taken on (a hash of the .so itself changes with every relink)."""
+    import glob
+
     h = hashlib.sha256()
-    with open(path, "rb") as f:
-        for b in iter(lambda: f.read(1 << 20), b""):
-            h.update(b)
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2605_00429_b200", "csrc", "cuda", "*.cu*")))
+    files += [os.path.join(ROOT, "include", "p2m.h"), os.path.join(ROOT, "Makefile")]
+    for p in files:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
     return h.hexdigest()
 
 
 def ncu_evidence(cfg, rows, sha):
     """DRAM traffic and pipe utilisation of the scan kernels from an ncu --set full capture of THIS
     build (profiles/*/ncu_scan_c{cfg}.json, written by scripts/ncu_scan_json.py, carries the
-    sha256 of the libp2m_cuda.so it profiled): used only if the hash and the row count match."""
+    sha256 of the CUDA sources it profiled): used only if the hash and the row count match."""
     import glob
 
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_scan_c{cfg}.json")), reverse=True):
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "**", f"ncu_scan_c{cfg}.json"), recursive=True), reverse=True):
         try:
             with open(p) as f:
                 d = json.load(f)
         except Exception:
             continue
-        if d.get("lib_sha256") == sha and int(d.get("rows", -1)) == int(rows):
+        if d.get("src_sha256") == sha and int(d.get("rows", -1)) == int(rows):
             d["file"] = os.path.relpath(p, ROOT)
             return d
     return None
@@ -506,7 +513,7 @@ def main():
     t_scan_s = split[4] / 1e3 if split[4] > 0 else ms / 1e3
     B_scan = ROW_BYTES * n + c["structure_bytes"]
     achieved = B_scan / t_scan_s / 1e9
-    sha = lib_sha256(os.path.join(ROOT, "paper_2605_00429_b200", "lib", "libp2m_cuda.so"))
+    sha = src_sha256()
     ev = ncu_evidence(cfg, n, sha)
     traffic = ev["dram_bytes_per_launch"] if ev else None
     compute = None

@@ -74,23 +74,32 @@ def spatial_bounds(key_counts, world: int):
     return np.maximum.accumulate(np.array(b))
 
 
-def spatial_shard(gen, n_total: int, world: int, rank: int, box, bits: int = 7, chunk: int = 1 << 23):
+def spatial_shard(gen, n_total: int, world: int, rank: int, box, bits: int = 7, chunk: int = 1 << 23,
+                  parts_per_rank: int = 1):
     """Rank `rank`'s rows of ONE batch under the Morton-range partition.  gen(first, count) yields rows
     [first, first+count) of the batch.  Two passes over the batch (key histogram, then selection);
-    returns (q rows of this rank in batch order, their batch row indices)."""
+    returns (q rows of this rank in batch order, their batch row indices).
+
+    parts_per_rank = k > 1 cuts the key order into world*k ranges of ~equal row counts and deals them
+    round-robin (rank r owns ranges r, r + world, ...): every range is still a compact region at the
+    batch's full row density (rows per site as in the single-GPU run), but a rank's time now averages
+    over k regions of the domain -- on c5 equal-row regions differ by up to 1.3x in scan time
+    (DESIGN.md section 8), which one range per rank turns into load imbalance."""
     if not (0 <= rank < world):
         raise ValueError("rank out of range")
+    if parts_per_rank < 1:
+        raise ValueError("parts_per_rank must be >= 1")
     counts = np.zeros(1 << (3 * bits), np.int64)
     for a in range(0, n_total, chunk):
         k = morton_keys(gen(a, min(chunk, n_total - a)), box, bits)
         counts += np.bincount(k.astype(np.int64), minlength=len(counts))
-    bnd = spatial_bounds(counts, world)
-    lo, hi = bnd[rank], bnd[rank + 1]
+    bnd = spatial_bounds(counts, world * parts_per_rank)
     qs, idx = [], []
     for a in range(0, n_total, chunk):
         q = gen(a, min(chunk, n_total - a))
         k = morton_keys(q, box, bits).astype(np.int64)
-        sel = np.flatnonzero((k >= lo) & (k < hi))
+        part = np.searchsorted(bnd, k, side="right") - 1
+        sel = np.flatnonzero(part % world == rank)
         qs.append(q[sel])
         idx.append(sel + a)
     if not qs:

@@ -1,7 +1,7 @@
 """Roofline evidence of the scan phase from one ncu --set full capture (scripts/gpu_prof_scan.sh):
 DRAM bytes, duration and pipe utilisation of k_scan_tiles + k_scan_small (the two kernels of one
 scan phase; ncu serialises them) -> profiles/<round>/ncu_scan_c<cfg>.json, tagged with the sha256
-of the libp2m_cuda.so that was profiled.  bench.py uses the file only when its own library has the
+of the CUDA sources that were profiled.  bench.py uses the file only when its own sources have the
 same hash and the row count matches (same build, same workload).
 
 usage: python scripts/ncu_scan_json.py REP CFG ROWS OUT.json [LIB]"""
@@ -12,6 +12,9 @@ import json
 import os
 import subprocess
 import sys
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import bench  # src_sha256: the hash bench.py matches the evidence against
 
 rep, cfg, rows, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 lib = sys.argv[5] if len(sys.argv) > 5 else os.path.join(os.path.dirname(__file__), "..", "paper_2605_00429_b200", "lib", "libp2m_cuda.so")
@@ -76,6 +79,7 @@ dram = sum(nz(b(d, "dram__bytes_read.sum")) + nz(b(d, "dram__bytes_write.sum")) 
 res = {
     "config": cfg, "rows": rows, "kernels": [d["Kernel Name"][:60] for d in ks],
     "lib_sha256": hashlib.sha256(open(lib, "rb").read()).hexdigest(),
+    "src_sha256": bench.src_sha256(),
     "gpu_time_s": T, "dram_bytes_per_launch": dram, "dram_gbs_under_ncu": dram / T / 1e9,
     "dram_pct": 100.0 * dram / T / 1e9 / PEAK,
     "l2_hit_pct": w("lts__t_sector_hit_rate.pct"),

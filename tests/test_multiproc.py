@@ -124,6 +124,18 @@ def test_spatial_partition_is_a_partition():
             assert len(idx) > 0.5 * len(pts) / world  # balanced up to key-cell granularity
         allidx = np.concatenate(seen)
         assert np.array_equal(np.sort(allidx), np.arange(len(pts)))
+        # several interleaved key ranges per rank (load balance): still a partition, still balanced,
+        # and every rank's rows are the union of whole key ranges dealt round-robin
+        seen = [shard.spatial_shard(gen, len(pts), world, r, box, bits=5, chunk=3000, parts_per_rank=4)[1]
+                for r in range(world)]
+        assert np.array_equal(np.sort(np.concatenate(seen)), np.arange(len(pts)))
+        assert all(len(i) > 0.5 * len(pts) / world for i in seen)
+        if world > 1:
+            k5 = shard.morton_keys(pts, box, 5).astype(np.int64)
+            bnd = shard.spatial_bounds(np.bincount(k5, minlength=1 << 15), world * 4)
+            part = np.searchsorted(bnd, k5, side="right") - 1
+            for r in range(world):
+                assert np.array_equal(np.unique(part[seen[r]]) % world, np.full(len(np.unique(part[seen[r]])), r))
     # the key ranges are contiguous: every key of part r is below every key of part r+1
     k = shard.morton_keys(pts, box, 5)
     q0, i0 = shard.spatial_shard(gen, len(pts), 2, 0, box, bits=5)
