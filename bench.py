@@ -9,8 +9,8 @@ Morton keys -> radix sort -> nearest-site descent -> regroup by site -> pruned l
 in input order (p2m_query_device on device-resident queries).
 
 Multi-GPU (torchrun, one process per GPU): STRONG scaling by default -- the one 100 M batch is
-sharded over the ranks (even contiguous slices, or --split spatial: Morton-range partitions so
-every GPU keeps the rows-per-site and L2 working set of a smaller spatial region); rank 0 builds
+sharded over the ranks (Morton-range partitions by default, so every GPU keeps the rows per site
+of the single-GPU run; --split even: contiguous slices); rank 0 builds
 the engine once and the other ranks load its EngineIndexFile.  No collective on the data path
 (barriers and the max-over-ranks step time only).
 
@@ -192,7 +192,7 @@ def build_engine(cfg, rank, world, build_threads, aux_corner_union, index_dir=No
     return V, F, h, info
 
 
-def rank_queries(cfg, V, F, rank, world, n_total, scaling, split, key_box):
+def rank_queries(cfg, V, F, rank, world, n_total, scaling, split, key_box, parts_per_rank=1):
     """This rank's rows of the batch: strong scaling shards ONE batch of n_total rows (even slices or
     Morton-range partitions), weak scaling gives every rank its own n_total rows."""
     import paper_2605_00429_b200 as P
@@ -209,8 +209,9 @@ def rank_queries(cfg, V, F, rank, world, n_total, scaling, split, key_box):
         desc = f"even slice [{first}, {first + count}) of the {n_total}-row batch"
     else:
         gen = lambda a, b: P.gen_queries(cfg, V, F, a, b)  # noqa: E731
-        q, idx = shard.spatial_shard(gen, n_total, world, rank, key_box)
-        desc = f"Morton-range part {rank}/{world} of the {n_total}-row batch ({len(q)} rows)"
+        q, idx = shard.spatial_shard(gen, n_total, world, rank, key_box, parts_per_rank=parts_per_rank)
+        desc = (f"Morton-range part {rank}/{world} ({parts_per_rank} interleaved ranges) of the "
+                f"{n_total}-row batch ({len(q)} rows)")
     return q, {"queries_s": round(time.perf_counter() - t0, 3), "rows": desc}
 
 
@@ -335,8 +336,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong (default): N GPUs share one batch; weak: every GPU gets a full batch")
-    ap.add_argument("--split", default="even", choices=["even", "spatial"],
-                    help="strong scaling: even contiguous slices or Morton-range (spatial) partitions")
+    ap.add_argument("--split", default="auto", choices=["auto", "even", "spatial"],
+                    help="strong scaling: even contiguous slices or Morton-range (spatial) partitions; "
+                         "auto = spatial for N > 1 (rows per site stay those of the 1-GPU run)")
+    ap.add_argument("--parts-per-rank", type=int, default=4,
+                    help="spatial split: Morton ranges per rank, dealt round-robin (load balance)")
     ap.add_argument("--index-dir", default=os.environ.get("P2M_INDEX_DIR", "/tmp/p2m_bench_index"),
                     help="N>1: where rank 0 writes the EngineIndexFile the other ranks load")
     ap.add_argument("--table-device", type=int, default=-1,
@@ -351,6 +355,8 @@ def main():
     ap.add_argument("--scan-mode", type=int, default=0, help="0 grouped (default), 1 fused per-row")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.split == "auto":
+        args.split = "spatial" if env_int("WORLD_SIZE", 1) > 1 and args.scaling == "strong" else "even"
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
@@ -393,7 +399,8 @@ def main():
     L.check(lib.p2m_set_scan_mode(eng.handle, args.scan_mode))
     arrays = h.arrays()
     key_box = shard.morton_box(arrays["site_xyz"][arrays["site_kind"] != 1])
-    q_host, tq = rank_queries(cfg, V, F, rank, world, n_total, args.scaling, args.split, key_box)
+    q_host, tq = rank_queries(cfg, V, F, rank, world, n_total, args.scaling, args.split, key_box,
+                              args.parts_per_rank)
     tb.update(tq)
     n = len(q_host)
 

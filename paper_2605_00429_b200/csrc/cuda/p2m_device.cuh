@@ -115,7 +115,8 @@ struct Params {
     // Voronoi cell box meets grid cell c is listed in grid_site[grid_off[c] .. grid_off[c+1])
     const D4* site_pos;     // by site id: {x, y, z, meta (sentinel bit)}
     const D4* site_ref;     // by site id: a point on the mesh {x, y, z, 1} or {.., .., .., 0} = none
-    int no_seed;            // 1: d_min starts at +inf in the grouped scan too (P2M_NO_SEED)
+    int no_seed;            // 0: every d_min seed; 1: d_min starts at +inf in the grouped scan too (P2M_NO_SEED);
+                            // 2: group-point seeds only, no per-row exact seed face (P2M_NO_DEEP_SEED)
     int no_batch;           // 1: no level-1 batch-sphere pruning (P2M_NO_BATCH)
     const uint32_t* grid_off;
     const uint32_t* grid_site;
@@ -123,6 +124,7 @@ struct Params {
     int tile_order;         // scan launch order: 0 site order, 1 longest-first, 2 list-length buckets
     uint32_t small_chunks;  // tiles of <= 32 rows and lists of <= this many chunks: one warp per tile (0: off)
     int warp_tiles;         // 1: every tile has <= 32 rows and is scanned by one warp (k_scan_small); no k_scan_tiles
+    int warp_queue;         // 1: warp tiles queue their (row, face) pairs and evaluate 32 at a time (k_scan_warpq)
     uint32_t warp_min_chunks;  // sites (not heavy) whose list has >= this many chunks get 32-row warp tiles (0: off, ~0: auto)
     unsigned long long* tile_trace;  // debug (P2M_TILE_TRACE): per tile {site, rows, list length, cycles | sm}
     const uint64_t* adj_off;  // Delaunay adjacency CSR (nullptr: no DelaunayWalk)

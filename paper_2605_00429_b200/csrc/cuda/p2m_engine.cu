@@ -348,7 +348,8 @@ struct Slot {
         Scratch sc;  // the chunk's pipeline scratch: persistent, so chunks on different streams never
                      // wait on each other through the stream-ordered allocator's reuse dependencies
     } ws[kPipe];
-    uint64_t cap = 0;
+    uint64_t cap = 0;   // rows per allocated staging set
+    int nsets = 0;      // staging sets allocated (ws[0 .. nsets))
     // pageable host buffers (p2m_query): pinned bounce rings, sub-chunks of kRows rows.  The calling
     // thread packs input sub-chunks into the in-ring (host memcpy) and enqueues their H2D copies; a
     // second thread enqueues the D2H copies of finished chunks into the out-ring and unpacks them into
@@ -383,6 +384,8 @@ struct p2m_engine {
                            // unchanged), 30 above (c5 at 100 M: the coarser order costs the scan more)
     int e2e_chunks = 0;
     double e2e_sched[4] = {1.0 / 32, 2.0, 0.25, 0.0};  // first, growth, cap, tail (P2M_E2E_SCHED)  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
+    bool e2e_sched_set = false;  // P2M_E2E_SCHED given: no automatic choice between the dense and sparse schedules
+    double e2e_sparse_tail = 0.125;  // sparse batches: one big chunk + a tail of this fraction (P2M_E2E_TAIL)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
     uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
@@ -594,14 +597,22 @@ int alloc_slot(Slot& s, const p2m_engine& E) {
 
 int ensure_scratch(Scratch& c, uint64_t n, uint64_t n_sites);
 
-int ensure_ws(Slot& s, uint64_t n, uint64_t n_sites) {
-    if (n <= s.cap) return P2M_OK;
+// Staging sets 0 .. nsets-1 of the host-API pipeline, each for chunks of up to n rows (a schedule of
+// c chunks only ever uses min(c, kPipe) sets: two big chunks must not pay for four).
+int ensure_ws(Slot& s, uint64_t n, uint64_t n_sites, int nsets) {
+    nsets = std::min(std::max(nsets, 1), (int)Slot::kPipe);
+    if (n <= s.cap && nsets <= s.nsets) return P2M_OK;
     CK(cudaDeviceSynchronize());
+    n = std::max(n, s.cap);
+    nsets = std::max(nsets, s.nsets);
     s.cap = 0;
-    for (auto& w : s.ws) {
+    s.nsets = 0;
+    for (int k = 0; k < Slot::kPipe; ++k) {
+        auto& w = s.ws[k];
         cudaFree(w.q); cudaFree(w.dist); cudaFree(w.cp); cudaFree(w.face); cudaFree(w.site); cudaFree(w.flags);
         free_scratch(w.sc);
         w = Slot::Ws{};
+        if (k >= nsets) continue;
         CK(cudaMalloc(&w.q, 24 * n));
         CK(cudaMalloc(&w.dist, 8 * n));
         CK(cudaMalloc(&w.cp, 24 * n));
@@ -612,6 +623,7 @@ int ensure_ws(Slot& s, uint64_t n, uint64_t n_sites) {
         if (rc != P2M_OK) return rc;
     }
     s.cap = n;
+    s.nsets = nsets;
     return P2M_OK;
 }
 
@@ -912,6 +924,7 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
         if (const char* v = std::getenv("P2M_TILE_ORDER")) s->params.tile_order = std::atoi(v);
         s->params.warp_tiles = 0;
         if (const char* v = std::getenv("P2M_SCAN_WARP")) s->params.warp_tiles = std::atoi(v) ? 1 : 0;
+        s->params.warp_queue = std::getenv("P2M_NO_WARP_QUEUE") ? 0 : 1;
         s->params.warp_min_chunks = ~0u;  // auto (run_pipeline)
         if (const char* v = std::getenv("P2M_WARP_MIN_CHUNKS")) s->params.warp_min_chunks = (uint32_t)std::max(0, std::atoi(v));
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;
@@ -922,7 +935,14 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
         double x[4];
         if (std::sscanf(v, "%lf,%lf,%lf,%lf", &x[0], &x[1], &x[2], &x[3]) == 4 && x[0] > 0 && x[1] >= 1 && x[2] > 0 &&
             x[3] >= 0 && x[3] < 1)
+        {
             for (int k = 0; k < 4; ++k) E->e2e_sched[k] = x[k];
+            E->e2e_sched_set = true;
+        }
+    }
+    if (const char* v = std::getenv("P2M_E2E_TAIL")) {
+        const double t = std::atof(v);
+        if (t >= 0 && t < 1) E->e2e_sparse_tail = t;
     }
     if (const char* v = std::getenv("P2M_E2E_CHUNKS")) E->e2e_chunks = std::max(0, std::atoi(v));
     return P2M_OK;
@@ -1190,7 +1210,7 @@ P2M_API int p2m_engine_create(const p2m_engine_desc* d, int n_devices, const int
             for (int c = 0; c < 3; ++c) { P.grid_lo[c] = grid.lo[c]; P.grid_inv[c] = grid.inv[c]; P.grid_res[c] = grid.res[c]; }
         }
         if (std::getenv("P2M_NO_GRID")) E->grid_cells = E->grid_pairs = 0;
-        P.no_seed = std::getenv("P2M_NO_SEED") ? 1 : 0;
+        P.no_seed = std::getenv("P2M_NO_SEED") ? 1 : std::getenv("P2M_NO_DEEP_SEED") ? 2 : 0;  // 2: group-point seeds only
         P.no_batch = std::getenv("P2M_NO_BATCH") ? 1 : 0;
     }
     std::vector<D4> site_pos(S), site_ref(S);
@@ -1697,6 +1717,16 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
                 const uint64_t k = (uint64_t)e->e2e_chunks;
                 const uint64_t c0 = std::max<uint64_t>(1ull << 16, (m + k - 1) / k);
                 for (uint64_t off = 0; off < m; off += c0) len_of.push_back(std::min(c0, m - off));
+            } else if (!e->e2e_sched_set && m < 128ull * e->n_sites && m >= (1ull << 22)) {
+                // Sparse batch (few rows per site, the regime of the warp tiles): a tile's cost is
+                // nearly independent of its rows, so every extra chunk re-pays the lists -- c5 at
+                // 100 M rows runs at 0.44 G rows/s whole, 0.38 in halves, 0.24 in eighths.  One big
+                // chunk and a small tail instead: the tail's H2D and the big chunk's D2H hide behind
+                // the other chunk's kernels, and the unhidden part is the big chunk's H2D (24 B/row)
+                // plus the tail's D2H.  Measured on c5: 402 ms (geometric) -> 329 (2 equal) -> ~300.
+                const uint64_t mt = std::max<uint64_t>(1ull << 18, (uint64_t)(e->e2e_sparse_tail * (double)m));
+                if (mt < m) { len_of.push_back(m - mt); len_of.push_back(mt); }
+                else len_of.push_back(m);
             } else {
                 // geometric: first chunk m*first, growing by `growth` up to m*cap, the last m*tail rows
                 // as a separate small chunk (its D2H is the pipeline's drain)
@@ -1720,7 +1750,7 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             }
             uint64_t maxlen = 0;
             for (uint64_t l : len_of) maxlen = std::max(maxlen, l);
-            int rc = ensure_ws(s, maxlen, e->n_sites);
+            int rc = ensure_ws(s, maxlen, e->n_sites, (int)len_of.size());
             if (rc != P2M_OK) return rc;
             if (cnt) {
                 CK(cudaMemsetAsync(s.agg, 0, sizeof(unsigned long long) * 8, s.pipe[0]));

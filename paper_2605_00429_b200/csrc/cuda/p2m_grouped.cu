@@ -287,15 +287,11 @@ __device__ __forceinline__ void staged_disk(const float* pf, int k, float4& r0, 
     r1 = make_float4(b[8], b[10], b[12], b[14]);
 }
 
-// One 32-entry batch staged in shared memory (disks: 16 pairs x 64 bytes, fid: 32 face ids), scanned
-// for this lane's row.  Called by every lane of the warp.
-template <bool kCounters>
-__device__ __forceinline__ void scan_batch_row(const Params& p, bool active, const V& q, uint64_t QX, uint64_t QY,
-                                               uint64_t QZ, uint64_t& DK, double& best, uint32_t& bf,
-                                               uint32_t& exact, unsigned long long& passes,
-                                               unsigned long long& rare_iters, unsigned long long& sbytes,
-                                               const float4* disk, const uint32_t* fid, int valid, int lane,
-                                               float* sdk) {
+// Level 2 of one staged batch for this lane's row: bit k of the result = candidate k's bounding disk may
+// hold a point within the row's d_min bound DK (conservative, branch-free f32x2).  Also tightens DK by
+// the nearest staged disk centre (a point of its face up to ctr_slack: an upper bound of the distance).
+__device__ __forceinline__ uint32_t batch_mask_row(const Params& p, bool active, uint64_t QX, uint64_t QY, uint64_t QZ,
+                                                   uint64_t& DK, const float4* disk, int valid, float* sdk) {
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
     const float Mq = row_scale(p, qxf, qyf, qzf);
     uint32_t mask = 0;
@@ -353,7 +349,7 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
         // every disk centre is a point of its face (up to ctr_slack): |q - c| bounds the row's distance
         // from above, so the nearest staged centre tightens d_min before the exact tests (padding
         // entries sit at 1e18, kPadDisk, and never count)
-        if (!p.no_seed) {
+        if (p.no_seed != 1) {
             const float dkf = dk_of(p, __fadd_ru(ub_of(smin, Mq), p.ctr_slack), Mq);
             if (dkf < dkx) {
                 DK = pk2(dkf, dkf);
@@ -361,6 +357,21 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
             }
         }
     }
+    return mask;
+}
+
+// One 32-entry batch staged in shared memory (disks: 16 pairs x 64 bytes, fid: 32 face ids), scanned
+// for this lane's row.  Called by every lane of the warp.
+template <bool kCounters>
+__device__ __forceinline__ void scan_batch_row(const Params& p, bool active, const V& q, uint64_t QX, uint64_t QY,
+                                               uint64_t QZ, uint64_t& DK, double& best, uint32_t& bf,
+                                               uint32_t& exact, unsigned long long& passes,
+                                               unsigned long long& rare_iters, unsigned long long& sbytes,
+                                               const float4* disk, const uint32_t* fid, int valid, int lane,
+                                               float* sdk) {
+    const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
+    const float Mq = row_scale(p, qxf, qyf, qzf);
+    const uint32_t mask = batch_mask_row(p, active, QX, QY, QZ, DK, disk, valid, sdk);
     uint32_t um = __reduce_or_sync(0xffffffffu, mask);
     if (kCounters) {
         passes += __popc(mask);
@@ -377,6 +388,7 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
             if (!cyl_near(qxf, qyf, qzf, __fmul_ru(dkx, dkx), r0, r1)) return false;
         }
         const uint32_t f = fid[kk];
+        if (f == bf) return false;               // the deep seed's face: already evaluated
         V a, bb3, c3, pp3;
         load_tri(p.rec + 4 * (uint64_t)f, &a, &bb3, &c3);
         const double dd = closest_tri(q, a, bb3, c3, &pp3);
@@ -410,13 +422,14 @@ __device__ __forceinline__ void scan_batch_row(const Params& p, bool active, con
 // (d^2, face id) argmin and every face that could tie it survive every prune).
 template <bool kCounters>
 __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q, uint64_t QX, uint64_t QY,
-                                         uint64_t QZ, double& dmin, uint64_t& DK) {
+                                         uint64_t QZ, double& dmin, uint64_t& DK, double& best, uint32_t& bf,
+                                         uint32_t& exact) {
     const float finf = __int_as_float(0x7f800000);
     const float qxf = __uint_as_float((uint32_t)QX), qyf = __uint_as_float((uint32_t)QY), qzf = __uint_as_float((uint32_t)QZ);
     const float Mq = row_scale(p, qxf, qyf, qzf);
     const uint64_t bo = p.boff[s], co = p.coff[s];
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
-    if (!p.no_seed) {
+    if (p.no_seed != 1) {
         // Seed d_min with an upper bound of the distance to the mesh: |q - ref| for a point ref ON
         // the mesh (the site itself for a mesh vertex, proj(s, M) for an auxiliary site).  A face
         // whose lower bound exceeds it (plus the prune slack) cannot attain or tie the minimum, so
@@ -429,7 +442,7 @@ __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q
             DK = pk2(dkf, dkf);
         }
     }
-    if (!p.no_seed && !p.no_batch) {
+    if (p.no_seed != 1 && !p.no_batch) {
         // Tighter seed: every chunk and batch carries a point P on the mesh near its centre
         // (p2m_engine.cu group_point), so |q - P| bounds the distance to the mesh from above.  fp32
         // with upward rounding: sqrt(d2f)*(1+1e-6) covers the rounding of d2f, delta the fp32
@@ -446,18 +459,63 @@ __device__ __forceinline__ void seed_row(const Params& p, uint32_t s, const V& q
         }
         const uint64_t nbl = p.boff[s + 1] - bo;
         const uint64_t bb0 = (uint64_t)bc * (kChunk / 32), bb1 = min(nbl, bb0 + kChunk / 32);
+        float ubb = finf;
+        uint64_t bbest = bb0;
         for (uint64_t b2 = bb0; b2 < bb1; ++b2) {
             const float4 c = p.bpt[bo + b2];
             const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
             const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            ub = fminf(ub, ub_of(d2f, Mq));
+            const float u = ub_of(d2f, Mq);
+            if (u < ubb) { ubb = u; bbest = b2; }
         }
+        ub = fminf(ub, ubb);
         if ((double)ub < dmin) {
             dmin = (double)ub;
             const float dkf = dk_of(p, ub, Mq);
             DK = pk2(dkf, dkf);
         }
+        if (p.no_seed == 0 && nbl) {
+            // Deep seed: the face of the row's best batch whose disk centre is nearest to q, evaluated
+            // exactly.  It is a face of this list, so (best, bf) starts at a genuine candidate of the
+            // argmin and d_min at its exact distance -- within the list's own tolerance of the final
+            // answer for most rows, so the chunk, batch and disk tests that follow prune against a
+            // near-final bound from the start, whatever order the tile visits the batches in (the
+            // best-first order serves the tile's first row only).  All 32 lanes evaluate at once.
+            const uint64_t e0 = p.off[s] + 32ull * bbest;
+            const int ne = (int)min((uint64_t)32, p.off[s + 1] - e0);
+            float sm = finf;
+            uint32_t fm = 0;
+#pragma unroll 4
+            for (int k = 0; k < ne; ++k) {
+                const uint32_t f = p.lfs[e0 + k];
+                const float4 c = p.fcy[kCy * (uint64_t)f];
+                const float dx = qxf - c.x, dy = qyf - c.y, dz = qzf - c.z;
+                const float d2f = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+                if (d2f < sm) { sm = d2f; fm = f; }
+            }
+            V a, b3, c3, pp3;
+            load_tri(p.rec + 4 * (uint64_t)fm, &a, &b3, &c3);
+            best = closest_tri(q, a, b3, c3, &pp3);
+            bf = fm;
+            ++exact;
+            const float dkf = dk_of(p, __fsqrt_ru(__double2float_ru(best)), Mq);
+            float dkx, dky;
+            upk2(DK, dkx, dky);
+            if (dkf < dkx) DK = pk2(dkf, dkf);
+        }
     }
+}
+
+// A deep-seeded row always holds a face, so "the list had no face within |q - ref(site)|" (a table that
+// is not a Theorem-1 superset, P2M_FLAG_TABLE_MISS) is detected from the result: ref lies ON the mesh,
+// so a superset list's minimum cannot exceed |q - ref| beyond rounding.
+__device__ __forceinline__ bool table_miss(const Params& p, uint32_t s, const V& q, double best, uint32_t bf) {
+    if (bf == 0xffffffffu) return true;
+    if (p.no_seed != 0) return false;
+    const D4 rf = ldg4(p.site_ref + s);
+    if (rf.w == 0.0) return false;
+    const double dr = vd2(q, V{rf.x, rf.y, rf.z});
+    return best > dr * (1.0 + 1e-9) + p.prune_eps * p.prune_eps;
 }
 
 // ---- warp tiles: one warp per tile of <= 32 rows --------------------------------------------
@@ -511,7 +569,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     uint32_t bf = 0xffffffffu, exact = 0;
     unsigned long long passes = 0, rare_iters = 0;
     unsigned long long sbytes = 0;               // structure bytes loaded (counters mode; bench roofline)
-    if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK);
+    if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK, best, bf, exact);
     const uint64_t beg = p.off[s], end = p.off[s + 1];
     const uint64_t bo = p.boff[s], co = p.coff[s];
     const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
@@ -612,7 +670,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
         o.cp[3 * (uint64_t)row + 1] = cp.y;
         o.cp[3 * (uint64_t)row + 2] = cp.z;
         o.face[row] = bf;
-        if (bf == 0xffffffffu && o.miss) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
+        if (o.miss && table_miss(p, s, q, best, bf)) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
         if (kCounters && o.per_query) {
             o.per_query[3 * (uint64_t)row] = end - beg;
             o.per_query[3 * (uint64_t)row + 1] = exact;
@@ -621,6 +679,261 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
     if (kCounters && o.agg) {
         unsigned long long v0 = active ? (end - beg) : 0ull, v1 = active ? exact : 0u, v2 = passes, v3 = rare_iters;
         unsigned long long v4 = sbytes + ((active && bf != 0xffffffffu) ? 96ull : 0ull);  // + the epilogue's record
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            v0 += __shfl_down_sync(0xffffffffu, v0, sh);
+            v1 += __shfl_down_sync(0xffffffffu, v1, sh);
+            v2 += __shfl_down_sync(0xffffffffu, v2, sh);
+            v3 += __shfl_down_sync(0xffffffffu, v3, sh);
+            v4 += __shfl_down_sync(0xffffffffu, v4, sh);
+        }
+        if (lane == 0) {
+            atomicAdd(o.agg + 0, v0);
+            atomicAdd(o.agg + 1, v1);
+            atomicAdd(o.agg + 4, v2);
+            atomicAdd(o.agg + 5, v3);
+            atomicAdd(o.agg + 6, v4);
+            atomicAdd(o.agg + 7, 1ull);
+        }
+    }
+}
+
+
+// ---- warp tiles with a queued exact path ------------------------------------------------------
+// Same tile walk as k_scan_small (windows of chunks, level-0/1 votes, best-first order, level-2 masks),
+// but the exact evaluations are not done batch by batch by "the lanes whose bit is set" -- on c5 that
+// runs the fp64 point-triangle kernel with ~4 of 32 lanes busy (profiles/r02).  Instead every
+// (row, face) pair that passes level 2 is appended to a per-warp queue in shared memory, and whenever
+// 32 pairs are queued the warp evaluates them one pair per lane, all lanes busy.  Each row's running
+// (d^2 bits, face id) minimum lives in shared memory; a round merges into it with two atomicMin steps
+// (d^2 first; then, among the pairs that attain the row's new d^2 -- plus the old face if d^2 did not
+// change -- the lowest face id): the lexicographic argmin, whatever the evaluation order.  Pairs wait
+// in the queue with the d_min of the moment they passed, which is only ever looser than the current
+// one: a queued face may be evaluated needlessly, never skipped wrongly.
+struct WarpQ {
+    double qx[32], qy[32], qz[32];               // the tile's rows (fp64)
+    unsigned long long best[32];                 // per row: bits of the smallest d^2 so far (+inf = none)
+    uint32_t bf[32];                             // ... and its face (lowest id among ties)
+    uint32_t ex[32];                             // per-row exact evaluations (counters mode)
+    uint32_t qf[64];                             // queue: face id ...
+    uint8_t qr[64];                              // ... and row lane of each waiting pair
+};
+
+template <bool kCounters>
+__global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, const double* __restrict__ q_xyz,
+                                                        const uint32_t* __restrict__ rows,
+                                                        const uint32_t* __restrict__ key,
+                                                        const uint32_t* __restrict__ tiles,
+                                                        const uint32_t* __restrict__ meta,
+                                                        const uint32_t* __restrict__ order, Out o) {
+    __shared__ float4 s_disk[kWarps][64];
+    __shared__ uint32_t s_fid[kWarps][32];
+    __shared__ WarpQ s_wq[kWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t nt = meta[0], ns = meta[2];
+    const uint32_t ti = blockIdx.x * kWarps + w;
+    if (ti >= ns) return;                        // warp-uniform: no block barrier in this kernel
+    float4* wd = s_disk[w];
+    uint32_t* wf = s_fid[w];
+    WarpQ& Q = s_wq[w];
+    const uint32_t b = order[nt - ns + ti];
+    const uint32_t start = tiles[b];
+    const uint32_t stop = (b + 1 < nt) ? tiles[b + 1] : meta[1];
+    const int m = (int)(stop - start);
+    const uint32_t s = key[start];
+    const bool active = lane < m;
+    const float finf = __int_as_float(0x7f800000);
+    uint32_t row = 0;
+    float fx = 0.f, fy = 0.f, fz = 0.f;
+    uint64_t DK = pk2(finf, finf);
+    uint32_t exact_seed = 0;
+    {
+        V q{0, 0, 0};
+        double best = __longlong_as_double(0x7ff0000000000000ll), dmin = best;
+        uint32_t bf = 0xffffffffu;
+        if (active) {
+            row = rows[start + lane];
+            q = V{q_xyz[3 * (uint64_t)row], q_xyz[3 * (uint64_t)row + 1], q_xyz[3 * (uint64_t)row + 2]};
+            fx = (float)q.x; fy = (float)q.y; fz = (float)q.z;
+            seed_row<kCounters>(p, s, q, pk2(fx, fx), pk2(fy, fy), pk2(fz, fz), dmin, DK, best, bf, exact_seed);
+        }
+        Q.qx[lane] = q.x; Q.qy[lane] = q.y; Q.qz[lane] = q.z;
+        Q.best[lane] = (unsigned long long)__double_as_longlong(best);
+        Q.bf[lane] = bf;
+        if (kCounters) Q.ex[lane] = exact_seed;
+    }
+    __syncwarp();
+    const float Mq = row_scale(p, fx, fy, fz);
+    const float rx = __shfl_sync(0xffffffffu, fx, 0), ry = __shfl_sync(0xffffffffu, fy, 0),
+                rz = __shfl_sync(0xffffffffu, fz, 0);  // the tile's first row: visiting order
+    unsigned long long passes = 0, rare_iters = 0;
+    unsigned long long sbytes = 0;               // structure bytes loaded (counters mode; bench roofline)
+    const uint64_t beg = p.off[s], end = p.off[s + 1];
+    const uint64_t bo = p.boff[s], co = p.coff[s];
+    const uint32_t nch = (uint32_t)(p.coff[s + 1] - co);
+    if (kCounters && lane == 0) sbytes += 16ull * nch + 76;  // chunk points, site ref, offsets, tile meta
+    auto near = [&](float4 c0, float4 c1) {
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        return cyl_near(fx, fy, fz, __fmul_ru(dkx, dkx), c0, c1);
+    };
+    auto bcast = [&](float4 v, int src) {
+        return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                           __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+    };
+    auto take_min = [&](uint32_t& k) {
+        const uint32_t mk = __reduce_min_sync(0xffffffffu, k);
+        const int src = __ffs(__ballot_sync(0xffffffffu, k == mk)) - 1;
+        if (lane == src) k = 0xffffffffu;
+        return src;
+    };
+    uint32_t qhead = 0, qn = 0;                  // queue window [qhead, qhead + qn) mod 64 (warp-uniform)
+    // one round: the first cnt (<= 32) queued pairs, one per lane, evaluated exactly and merged
+    auto round = [&](uint32_t cnt) {
+        const bool has = (uint32_t)lane < cnt;
+        uint32_t f = 0;
+        int r = 0;
+        if (has) { f = Q.qf[(qhead + lane) & 63u]; r = Q.qr[(qhead + lane) & 63u]; }
+        const unsigned long long old = Q.best[lane];
+        const bool ev = has && f != Q.bf[r];     // the row's current face (the deep seed's) is done already
+        unsigned long long kd = ~0ull;
+        if (ev) {
+            const V qr{Q.qx[r], Q.qy[r], Q.qz[r]};
+            V a, b3, c3, pp3;
+            load_tri(p.rec + 4 * (uint64_t)f, &a, &b3, &c3);
+            kd = (unsigned long long)__double_as_longlong(closest_tri(qr, a, b3, c3, &pp3));  // d^2 >= +0: bits order as values
+        }
+        __syncwarp();                            // every lane has read old / bf before the merge
+        if (ev) atomicMin(&Q.best[r], kd);
+        __syncwarp();
+        const unsigned long long nk = Q.best[lane];
+        if (nk != old) Q.bf[lane] = 0xffffffffu; // a strictly smaller d^2: only its faces count
+        __syncwarp();
+        if (ev && kd == Q.best[r]) atomicMin(&Q.bf[r], f);
+        if (kCounters) {
+            if (ev) atomicAdd(&Q.ex[r], 1u);
+            const uint32_t nev = __popc(__ballot_sync(0xffffffffu, ev));
+            if (lane == 0) { rare_iters += 32; sbytes += 96ull * nev; }
+        }
+        __syncwarp();
+        if (nk != old) {
+            // any upper bound of sqrt(best) is a valid d_min: the fp32 sqrt rounded up of best rounded up
+            const float dkf = dk_of(p, __fsqrt_ru(__double2float_ru(__longlong_as_double((long long)nk))), Mq);
+            float dkx, dky;
+            upk2(DK, dkx, dky);
+            if (dkf < dkx) DK = pk2(dkf, dkf);
+        }
+        qhead = (qhead + cnt) & 63u;
+        qn -= cnt;
+    };
+    float* wdf = reinterpret_cast<float*>(wd);
+    for (uint32_t w0 = 0; w0 < nch; w0 += 32) {
+        const int wn = (int)min(32u, nch - w0);
+        float4 cc0 = make_float4(0.f, 0.f, 0.f, 0.f), cc1 = cc0;  // lane k: chunk w0 + k's cylinder
+        if (lane < wn) { cc0 = p.ccy[kCy * (co + w0 + lane)]; cc1 = p.ccy[kCy * (co + w0 + lane) + 1]; }
+        if (kCounters && lane == 0) sbytes += 32ull * wn;
+        uint32_t cneed = 0;
+        if (nch == 1 || p.no_batch) {
+            cneed = wn == 32 ? 0xffffffffu : ((1u << wn) - 1u);
+        } else {
+            for (int k = 0; k < wn; ++k) {
+                const float4 c0 = bcast(cc0, k), c1 = bcast(cc1, k);
+                if (__any_sync(0xffffffffu, active && near(c0, c1))) cneed |= 1u << k;
+            }
+        }
+        const int nn = __popc(cneed);
+        uint32_t ckey = ((cneed >> lane) & 1u) ? (nn > 1 ? cyl_key(rx, ry, rz, cc0, cc1) : 0u) : 0xffffffffu;
+        for (int pos = 0; pos < nn; ++pos) {
+            const int src = take_min(ckey);
+            const uint32_t cidx = w0 + (uint32_t)src;
+            if (pos > 0 && !p.no_batch) {
+                const float4 c0 = bcast(cc0, src), c1 = bcast(cc1, src);
+                if (!__any_sync(0xffffffffu, active && near(c0, c1))) continue;
+            }
+            const uint64_t cb = beg + (uint64_t)cidx * kChunk;
+            const int nb = (int)((min((uint64_t)kChunk, end - cb) + 31) >> 5);
+            if (kCounters && lane == 0) sbytes += 32ull * nb;
+            float4 b0c = make_float4(0.f, 0.f, 0.f, 0.f), b1c = b0c;
+            uint32_t bk = 0xffffffffu;
+            if (lane < nb) {
+                const uint64_t gi = kCy * (bo + (uint64_t)cidx * (kChunk / 32) + lane);
+                b0c = p.bcy[gi];
+                b1c = p.bcy[gi + 1];
+                bk = nb > 1 ? cyl_key(rx, ry, rz, b0c, b1c) : 0u;
+            }
+            for (int bpos = 0; bpos < nb; ++bpos) {
+                const int bsrc = take_min(bk);
+                if (!p.no_batch) {
+                    const float4 c0 = bcast(b0c, bsrc), c1 = bcast(b1c, bsrc);
+                    if (!__any_sync(0xffffffffu, active && near(c0, c1))) continue;  // pruned whole
+                }
+                const uint64_t b0 = cb + 32ull * bsrc;
+                const int valid = (int)min((uint64_t)32, end - b0);
+                uint32_t f = 0;
+                float4 r0 = kPadDisk, r1 = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (lane < valid) { f = p.lfs[b0 + lane]; r0 = p.fcy[kCy * (uint64_t)f]; r1 = p.fcy[kCy * (uint64_t)f + 1]; }
+                wf[lane] = f;
+                stage_disk(wdf, lane, r0, r1);
+                __syncwarp();
+                if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
+                uint32_t mask = batch_mask_row(p, active, pk2(fx, fx), pk2(fy, fy), pk2(fz, fz), DK, wd, valid, nullptr);
+                if (kCounters) passes += __popc(mask);
+                // append this batch's (row, face) pairs to the queue, in lane order, as many as fit; a
+                // full warp's worth is evaluated as soon as it is there
+                while (__any_sync(0xffffffffu, mask != 0u)) {
+                    const uint32_t cnt = __popc(mask);
+                    uint32_t incl = cnt;
+#pragma unroll
+                    for (int sh = 1; sh < 32; sh <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, sh);
+                        if (lane >= sh) incl += v;
+                    }
+                    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                    const uint32_t space = 64u - qn;
+                    uint32_t wpos = incl - cnt;
+                    while (mask && wpos < space) {
+                        const int k = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        const uint32_t slot = (qhead + qn + wpos) & 63u;
+                        Q.qf[slot] = wf[k];
+                        Q.qr[slot] = (uint8_t)lane;
+                        ++wpos;
+                    }
+                    qn += min(total, space);
+                    __syncwarp();
+                    while (qn >= 32u) round(32u);
+                }
+                __syncwarp();                    // the slice is rewritten by the next batch
+            }
+        }
+    }
+    if (qn) round(qn);
+    __syncwarp();
+    if (active) {
+        const V q{Q.qx[lane], Q.qy[lane], Q.qz[lane]};
+        const double best = __longlong_as_double((long long)Q.best[lane]);
+        const uint32_t bf = Q.bf[lane];
+        V cp{__longlong_as_double(0x7ff8000000000000ll), __longlong_as_double(0x7ff8000000000000ll),
+             __longlong_as_double(0x7ff8000000000000ll)};
+        if (bf != 0xffffffffu) {
+            V a, bb, c;
+            load_tri(p.rec + 4 * (uint64_t)bf, &a, &bb, &c);
+            closest_tri(q, a, bb, c, &cp);
+        }
+        o.dist[row] = sqrt(best);
+        o.cp[3 * (uint64_t)row] = cp.x;
+        o.cp[3 * (uint64_t)row + 1] = cp.y;
+        o.cp[3 * (uint64_t)row + 2] = cp.z;
+        o.face[row] = bf;
+        if (o.miss && table_miss(p, s, q, best, bf)) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
+        if (kCounters && o.per_query) {
+            o.per_query[3 * (uint64_t)row] = end - beg;
+            o.per_query[3 * (uint64_t)row + 1] = Q.ex[lane];
+        }
+    }
+    if (kCounters && o.agg) {
+        unsigned long long v0 = active ? (end - beg) : 0ull, v1 = active ? Q.ex[lane] : 0u, v2 = passes, v3 = rare_iters;
+        unsigned long long v4 = sbytes + ((active && Q.bf[lane] != 0xffffffffu) ? 96ull : 0ull);  // + the epilogue's record
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) {
             v0 += __shfl_down_sync(0xffffffffu, v0, sh);
@@ -730,7 +1043,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         pre_c = 0;
     }
 #endif
-    if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK);
+    if (active) seed_row<kCounters>(p, s, q, QX, QY, QZ, dmin, DK, best, bf, exact);
     if (active && r == 0) {                      // replicas share one pruning bound per row
         float dkx, dky;
         upk2(DK, dkx, dky);
@@ -988,7 +1301,7 @@ __global__ void __launch_bounds__(kTile, P2M_SCAN_MINB) k_scan_tiles(Params p, c
         o.cp[3 * (uint64_t)row + 1] = cp.y;
         o.cp[3 * (uint64_t)row + 2] = cp.z;
         o.face[row] = bf;
-        if (bf == 0xffffffffu && o.miss) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
+        if (o.miss && table_miss(p, s, q, best, bf)) o.miss[atomicAdd(o.miss_n, 1u)] = row;  // not a superset: fallback
         if (kCounters && o.per_query) {
             o.per_query[3 * (uint64_t)row] = end - beg;
             o.per_query[3 * (uint64_t)row + 1] = exact;
@@ -1156,6 +1469,19 @@ cudaError_t launch_tile_order(const Params& p, const uint32_t* key, const uint32
     return cub::DeviceRadixSort::SortPairsDescending(tmp, tb, tkey, tkey2, tidx, order, (int64_t)max_t, 0, bits, s);
 }
 
+// the warp-tile kernel: queued exact path (default) or the batch-by-batch union walk (P2M_NO_WARP_QUEUE)
+static void launch_warp_tiles(const Params& p, const double* q, const uint32_t* rows, const uint32_t* key,
+                              const uint32_t* tiles, const uint32_t* meta, const uint32_t* order, const Out& o,
+                              bool counters, unsigned gs, cudaStream_t s) {
+    if (p.warp_queue) {
+        if (counters) k_scan_warpq<true><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_warpq<false><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+    } else {
+        if (counters) k_scan_small<true><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+        else k_scan_small<false><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+    }
+}
+
 cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* rows, const uint32_t* key,
                               const uint32_t* tiles, const uint32_t* meta, const uint32_t* order, uint64_t n,
                               const Out& o, bool counters, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
@@ -1166,8 +1492,7 @@ cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* 
     cudaError_t e;
     if (p.warp_tiles) {                          // warp mode: every tile is a warp tile
         const unsigned gs = (g + kWarps - 1) / kWarps;
-        if (counters) k_scan_small<true><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
-        else k_scan_small<false><<<gs, kTile, 0, s>>>(p, q, rows, key, tiles, meta, order, o);
+        launch_warp_tiles(p, q, rows, key, tiles, meta, order, o, counters, gs, s);
         return cudaGetLastError();
     }
     // warp tiles (small lists, or every non-heavy site in sparse batches): k_scan_small, on a side
@@ -1182,8 +1507,7 @@ cudaError_t launch_scan_tiles(const Params& p, const double* q, const uint32_t* 
             ss = side;
         }
         const unsigned gs = (g + kWarps - 1) / kWarps;
-        if (counters) k_scan_small<true><<<gs, kTile, 0, ss>>>(p, q, rows, key, tiles, meta, order, o);
-        else k_scan_small<false><<<gs, kTile, 0, ss>>>(p, q, rows, key, tiles, meta, order, o);
+        launch_warp_tiles(p, q, rows, key, tiles, meta, order, o, counters, gs, ss);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (fork_side && (e = cudaEventRecord(join, side)) != cudaSuccess) return e;
     }

@@ -25,7 +25,7 @@ kern = []
 for row in rr[2:]:
     d = dict(zip(hdr, row))
     name = d.get("Kernel Name", "")
-    if "k_scan_tiles" in name or "k_scan_small" in name:
+    if "k_scan_tiles" in name or "k_scan_small" in name or "k_scan_warpq" in name:
         kern.append(d)
 if not kern:
     sys.exit("no scan kernels in " + rep)

@@ -42,3 +42,7 @@ tot = sum(a[0] for a in agg) or 1
 print(f"  hottest source lines by warp-stall samples ({tot} samples):")
 for a in sorted(agg, reverse=True)[:top]:
     print(f"    {100 * a[0] / tot:5.1f}%  {a[1]}:{a[2]:<5d} inst {a[4] / 1e6:7.1f}M  {a[3]}")
+toti = sum(a[4] for a in agg) or 1
+print(f"  most executed source lines (warp instructions, {toti / 1e9:.1f} G attributed):")
+for a in sorted(agg, key=lambda x: -x[4])[:top]:
+    print(f"    {100 * a[4] / toti:5.1f}%  {a[1]}:{a[2]:<5d} inst {a[4] / 1e6:7.1f}M  stall {100 * a[0] / tot:4.1f}%  {a[3]}")

@@ -320,6 +320,9 @@ def test_host_api_chunk_schedules_identical(c2, chunks, monkeypatch):
     {"P2M_LONG_TILE": "128"},                  # heavy-site tile height
     {"P2M_HEAVY_E": "16"},                     # many more heavy sites (short tiles)
     {"P2M_NO_SEED": "1"}, {"P2M_NO_BATCH": "1"},  # without the d_min seeds / group-sphere levels
+    {"P2M_NO_DEEP_SEED": "1"},                 # group-point seeds only (no per-row exact seed face)
+    {"P2M_NO_WARP_QUEUE": "1"},                # warp tiles evaluate batch by batch (union walk), no pair queue
+    {"P2M_NO_WARP_QUEUE": "1", "P2M_SCAN_WARP": "1"},
     {"P2M_NO_SPATIAL": "1"},                   # lists scanned in ascending face order
     {"P2M_SCAN_WARP": "1"},                    # every tile a 32-row warp tile (no CTA tiles)
     {"P2M_WARP_MIN_CHUNKS": "0"},              # no warp tiles beyond the small-list ones
