@@ -339,7 +339,7 @@ def main():
     ap.add_argument("--split", default="auto", choices=["auto", "even", "spatial"],
                     help="strong scaling: even contiguous slices or Morton-range (spatial) partitions; "
                          "auto = spatial for N > 1 (rows per site stay those of the 1-GPU run)")
-    ap.add_argument("--parts-per-rank", type=int, default=4,
+    ap.add_argument("--parts-per-rank", type=int, default=8,
                     help="spatial split: Morton ranges per rank, dealt round-robin (load balance)")
     ap.add_argument("--index-dir", default=os.environ.get("P2M_INDEX_DIR", "/tmp/p2m_bench_index"),
                     help="N>1: where rank 0 writes the EngineIndexFile the other ranks load")

@@ -385,7 +385,7 @@ struct p2m_engine {
     int e2e_chunks = 0;
     double e2e_sched[4] = {1.0 / 32, 2.0, 0.25, 0.0};  // first, growth, cap, tail (P2M_E2E_SCHED)  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
     bool e2e_sched_set = false;  // P2M_E2E_SCHED given: no automatic choice between the dense and sparse schedules
-    double e2e_sparse_tail = 0.125;  // sparse batches: one big chunk + a tail of this fraction (P2M_E2E_TAIL)
+    double e2e_sparse_tail = 0.5;  // sparse batches: one big chunk + a tail of this fraction (P2M_E2E_TAIL)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
     uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
@@ -1722,8 +1722,9 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
                 // nearly independent of its rows, so every extra chunk re-pays the lists -- c5 at
                 // 100 M rows runs at 0.44 G rows/s whole, 0.38 in halves, 0.24 in eighths.  One big
                 // chunk and a small tail instead: the tail's H2D and the big chunk's D2H hide behind
-                // the other chunk's kernels, and the unhidden part is the big chunk's H2D (24 B/row)
-                // plus the tail's D2H.  Measured on c5: 402 ms (geometric) -> 329 (2 equal) -> ~300.
+                // the other chunk's kernels.  Measured (100 M rows, pinned): c5 358 ms geometric, 306 in
+                // two halves, 296 at 80/20; c4 (kernels as fast as the copies) 199 geometric, 170 in two
+                // halves, 219 at 80/20 -- halves are the robust choice (P2M_E2E_TAIL sets the fraction).
                 const uint64_t mt = std::max<uint64_t>(1ull << 18, (uint64_t)(e->e2e_sparse_tail * (double)m));
                 if (mt < m) { len_of.push_back(m - mt); len_of.push_back(mt); }
                 else len_of.push_back(m);

@@ -881,16 +881,19 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, co
                 // append this batch's (row, face) pairs to the queue, in lane order, as many as fit; a
                 // full warp's worth is evaluated as soon as it is there
                 while (__any_sync(0xffffffffu, mask != 0u)) {
+                    // exclusive prefix of the lanes' pair counts by bit planes (counts are small: one or
+                    // two ballots instead of a five-step shuffle scan)
                     const uint32_t cnt = __popc(mask);
-                    uint32_t incl = cnt;
-#pragma unroll
-                    for (int sh = 1; sh < 32; sh <<= 1) {
-                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, sh);
-                        if (lane >= sh) incl += v;
+                    const uint32_t planes = __reduce_or_sync(0xffffffffu, cnt);
+                    const uint32_t lt = (1u << lane) - 1u;
+                    uint32_t wpos = 0, total = 0;
+                    for (uint32_t bit = 1u; bit <= planes; bit <<= 1) {
+                        if (!(planes & bit)) continue;
+                        const uint32_t bl = __ballot_sync(0xffffffffu, (cnt & bit) != 0u);
+                        wpos += bit * __popc(bl & lt);
+                        total += bit * __popc(bl);
                     }
-                    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
                     const uint32_t space = 64u - qn;
-                    uint32_t wpos = incl - cnt;
                     while (mask && wpos < space) {
                         const int k = __ffs(mask) - 1;
                         mask &= mask - 1;
