@@ -124,6 +124,7 @@ struct Params {
     int tile_order;         // scan launch order: 0 site order, 1 longest-first, 2 list-length buckets
     uint32_t small_chunks;  // tiles of <= 32 rows and lists of <= this many chunks: one warp per tile (0: off)
     int warp_tiles;         // 1: every tile has <= 32 rows and is scanned by one warp (k_scan_small); no k_scan_tiles
+    int tvote;              // 1: k_scan_warpq votes on chunks / batches lane-parallel over the groups (P2M_NO_TVOTE: 0)
     int warp_queue;         // 1: warp tiles queue their (row, face) pairs and evaluate 32 at a time (k_scan_warpq)
     uint32_t warp_min_chunks;  // sites (not heavy) whose list has >= this many chunks get 32-row warp tiles (0: off, ~0: auto)
     unsigned long long* tile_trace;  // debug (P2M_TILE_TRACE): per tile {site, rows, list length, cycles | sm}

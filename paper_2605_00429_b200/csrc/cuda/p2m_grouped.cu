@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_small(Params p, co
 // in the queue with the d_min of the moment they passed, which is only ever looser than the current
 // one: a queued face may be evaluated needlessly, never skipped wrongly.
 struct WarpQ {
+    float4 row[32];                              // the tile's rows (fp32) and their squared bounds: group votes
     double qx[32], qy[32], qz[32];               // the tile's rows (fp64)
     unsigned long long best[32];                 // per row: bits of the smallest d^2 so far (+inf = none)
     uint32_t bf[32];                             // ... and its face (lowest id among ties)
@@ -761,6 +762,7 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, co
         Q.best[lane] = (unsigned long long)__double_as_longlong(best);
         Q.bf[lane] = bf;
         if (kCounters) Q.ex[lane] = exact_seed;
+        Q.row[lane] = make_float4(fx, fy, fz, 0.f);
     }
     __syncwarp();
     const float Mq = row_scale(p, fx, fy, fz);
@@ -786,6 +788,14 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, co
         const int src = __ffs(__ballot_sync(0xffffffffu, k == mk)) - 1;
         if (lane == src) k = 0xffffffffu;
         return src;
+    };
+    // the rows' current squared bounds for the transposed votes
+    auto publish_bounds = [&]() {
+        float dkx, dky;
+        upk2(DK, dkx, dky);
+        __syncwarp();
+        Q.row[lane].w = __fmul_ru(dkx, dkx);
+        __syncwarp();
     };
     uint32_t qhead = 0, qn = 0;                  // queue window [qhead, qhead + qn) mod 64 (warp-uniform)
     // one round: the first cnt (<= 32) queued pairs, one per lane, evaluated exactly and merged
@@ -835,6 +845,19 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, co
         uint32_t cneed = 0;
         if (nch == 1 || p.no_batch) {
             cneed = wn == 32 ? 0xffffffffu : ((1u << wn) - 1u);
+        } else if (p.tvote) {
+            // transposed vote: lane k holds chunk k's cylinder and walks the tile's rows (shared memory,
+            // broadcast reads) until one of them may need the chunk -- m row tests for the whole window
+            // instead of a broadcast + test + vote per chunk; the same predicate on the same operands
+            publish_bounds();
+            bool need = false;
+            if (lane < wn) {
+                for (int r = 0; r < m; ++r) {
+                    const float4 rw = Q.row[r];
+                    if (cyl_near(rw.x, rw.y, rw.z, rw.w, cc0, cc1)) { need = true; break; }
+                }
+            }
+            cneed = __ballot_sync(0xffffffffu, need);
         } else {
             for (int k = 0; k < wn; ++k) {
                 const float4 c0 = bcast(cc0, k), c1 = bcast(cc1, k);
@@ -861,9 +884,27 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, co
                 b1c = p.bcy[gi + 1];
                 bk = nb > 1 ? cyl_key(rx, ry, rz, b0c, b1c) : 0u;
             }
-            for (int bpos = 0; bpos < nb; ++bpos) {
+            int nbv = nb;
+            if (p.tvote && !p.no_batch) {
+                // transposed pre-vote over the chunk's batches: lane L tests batch L & 7 against the rows
+                // L >> 3, L >> 3 + 4, ...; a batch no row may need is never selected below
+                publish_bounds();
+                const float4 t0 = bcast(b0c, lane & 7), t1 = bcast(b1c, lane & 7);
+                bool need = false;
+                if ((lane & 7) < nb) {
+                    for (int r = lane >> 3; r < m; r += 4) {
+                        const float4 rw = Q.row[r];
+                        if (cyl_near(rw.x, rw.y, rw.z, rw.w, t0, t1)) { need = true; break; }
+                    }
+                }
+                uint32_t bn = __ballot_sync(0xffffffffu, need);
+                bn = (bn | (bn >> 8) | (bn >> 16) | (bn >> 24)) & 0xffu;
+                if (!((bn >> lane) & 1u)) bk = 0xffffffffu;
+                nbv = __popc(bn);
+            }
+            for (int bpos = 0; bpos < nbv; ++bpos) {
                 const int bsrc = take_min(bk);
-                if (!p.no_batch) {
+                if (!p.no_batch && !(p.tvote && bpos == 0)) {   // (the pre-vote just held for the first one)
                     const float4 c0 = bcast(b0c, bsrc), c1 = bcast(b1c, bsrc);
                     if (!__any_sync(0xffffffffu, active && near(c0, c1))) continue;  // pruned whole
                 }
