@@ -511,7 +511,7 @@ def main():
         return
 
     peak, peak_src = peaks()
-    # Roofline of the dominant kernel (the scan phase: k_scan_tiles || k_scan_small).  Algorithmic
+    # Roofline of the dominant kernel (the scan phase: k_scan_warpq || k_scan_tiles).  Algorithmic
     # bytes per launch = 64 B per row (q + row index in, distance + closest point + face out) + the
     # structure bytes the scan kernels load, counted by the kernels themselves in the counters pass:
     # each staged batch (face ids + face disks) once per tile or warp tile, group records once per
@@ -554,13 +554,14 @@ def main():
             "split_ms": {"morton": split[0], "sort": split[1], "descend": split[2], "regroup_sort": split[3], "scan": split[4], "total": split[5]},
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "scan phase: k_scan_tiles || k_scan_small (site-tiled pruned list scan, exact fp64)",
+                     "traffic": traffic, "kernel": "scan phase: k_scan_warpq || k_scan_tiles (site-tiled pruned list scan, exact fp64)",
                      "algorithmic_bytes_per_launch": B_scan,
                      "bytes_model": "64 B/row (q, row index, distance, closest point, face) + the structure bytes the "
                                     "scan kernels load, counted in-kernel: per tile the list's chunk points and "
                                     "cylinders (16 + 32 B per chunk) and 76 B of offsets/meta; per visited chunk its "
                                     "batch cylinders (32 B each); per staged batch 36 B/entry (face id + face disk); "
-                                    "96 B face record per exact test",
+                                    "96 B face record per exact evaluation (per queued pair on the warp-tile path, per warp "
+                                    "visit on the CTA path)",
                      "measured_dram_gbs": (traffic / t_scan_s / 1e9) if traffic else None,
                      "compute": compute,
                      "peak_source": peak_src},

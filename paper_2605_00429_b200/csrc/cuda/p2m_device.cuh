@@ -125,6 +125,8 @@ struct Params {
     uint32_t small_chunks;  // tiles of <= 32 rows and lists of <= this many chunks: one warp per tile (0: off)
     int warp_tiles;         // 1: every tile has <= 32 rows and is scanned by one warp (k_scan_small); no k_scan_tiles
     int tvote;              // 1: k_scan_warpq votes on chunks / batches lane-parallel over the groups (P2M_NO_TVOTE: 0)
+    uint32_t dense_pairs;   // k_scan_warpq: a batch whose rows average >= this many per wanted face walks the union
+                            // of their masks (broadcast record reads) instead of queueing the pairs (P2M_DENSE_PAIRS)
     int warp_queue;         // 1: warp tiles queue their (row, face) pairs and evaluate 32 at a time (k_scan_warpq)
     uint32_t warp_min_chunks;  // sites (not heavy) whose list has >= this many chunks get 32-row warp tiles (0: off, ~0: auto)
     unsigned long long* tile_trace;  // debug (P2M_TILE_TRACE): per tile {site, rows, list length, cycles | sm}

@@ -926,6 +926,8 @@ int upload_engine(p2m_engine* E, const Params& P, const Image& I, int n_devices,
         if (const char* v = std::getenv("P2M_SCAN_WARP")) s->params.warp_tiles = std::atoi(v) ? 1 : 0;
         s->params.warp_queue = std::getenv("P2M_NO_WARP_QUEUE") ? 0 : 1;
         s->params.tvote = std::getenv("P2M_NO_TVOTE") ? 0 : 1;
+        s->params.dense_pairs = 12u;
+        if (const char* v = std::getenv("P2M_DENSE_PAIRS")) s->params.dense_pairs = (uint32_t)std::max(1, std::atoi(v));
         s->params.warp_min_chunks = ~0u;  // auto (run_pipeline)
         if (const char* v = std::getenv("P2M_WARP_MIN_CHUNKS")) s->params.warp_min_chunks = (uint32_t)std::max(0, std::atoi(v));
         s->params.adj_off = E->has_adj ? s->adj_off : nullptr;

@@ -919,6 +919,47 @@ __global__ void __launch_bounds__(256, P2M_SMALL_MINB) k_scan_warpq(Params p, co
                 if (kCounters && lane == 0) sbytes += 36ull * valid;  // staged ids + disks
                 uint32_t mask = batch_mask_row(p, active, pk2(fx, fx), pk2(fy, fy), pk2(fz, fz), DK, wd, valid, nullptr);
                 if (kCounters) passes += __popc(mask);
+                // Dense batch -- the rows want the same faces (a flat distance field: c3's cylinder axis,
+                // where ~25 rows share each candidate): walk the union of the masks instead, so that one
+                // broadcast read of a face record serves every row that needs it.  Queued, those pairs
+                // would gather one record per lane (c3: 10.6 kB of records per query against 0.9, and
+                // half the rate).  Sparse batches (c5: ~4 rows per candidate) go to the queue.
+                {
+                    uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+                    const uint32_t npairs = __reduce_add_sync(0xffffffffu, __popc(mask));
+                    if (npairs >= p.dense_pairs * __popc(um) && um) {
+                        if (kCounters && lane == 0) rare_iters += 32u * __popc(um);
+                        while (um) {
+                            const int kk = __ffs(um) - 1;
+                            um &= um - 1;
+                            bool ex = false;
+                            if ((mask >> kk) & 1u) {
+                                float dkx, dky;
+                                upk2(DK, dkx, dky);
+                                float4 r0, r1;
+                                staged_disk(wdf, kk, r0, r1);
+                                const uint32_t f = wf[kk];
+                                if (cyl_near(fx, fy, fz, __fmul_ru(dkx, dkx), r0, r1) && f != Q.bf[lane]) {
+                                    const V qr{Q.qx[lane], Q.qy[lane], Q.qz[lane]};
+                                    V a, b3, c3, pp3;
+                                    load_tri(p.rec + 4 * (uint64_t)f, &a, &b3, &c3);
+                                    const double dd = closest_tri(qr, a, b3, c3, &pp3);
+                                    const double best = __longlong_as_double((long long)Q.best[lane]);
+                                    ex = true;
+                                    if (kCounters) ++Q.ex[lane];
+                                    if (dd < best || (dd == best && f < Q.bf[lane])) {   // this lane owns its row's slots
+                                        Q.best[lane] = (unsigned long long)__double_as_longlong(dd);
+                                        Q.bf[lane] = f;
+                                        const float dkf = dk_of(p, __fsqrt_ru(__double2float_ru(dd)), Mq);
+                                        if (dkf < dkx) DK = pk2(dkf, dkf);
+                                    }
+                                }
+                            }
+                            if (kCounters && __any_sync(0xffffffffu, ex) && lane == 0) sbytes += 96;
+                        }
+                        mask = 0u;
+                    }
+                }
                 // append this batch's (row, face) pairs to the queue, in lane order, as many as fit; a
                 // full warp's worth is evaluated as soon as it is there
                 while (__any_sync(0xffffffffu, mask != 0u)) {

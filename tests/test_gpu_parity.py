@@ -323,6 +323,7 @@ def test_host_api_chunk_schedules_identical(c2, chunks, monkeypatch):
     {"P2M_NO_DEEP_SEED": "1"},                 # group-point seeds only (no per-row exact seed face)
     {"P2M_NO_WARP_QUEUE": "1"},                # warp tiles evaluate batch by batch (union walk), no pair queue
     {"P2M_NO_WARP_QUEUE": "1", "P2M_SCAN_WARP": "1"},
+    {"P2M_DENSE_PAIRS": "1"}, {"P2M_DENSE_PAIRS": "1000"},  # warp tiles: every batch walks the union / queues its pairs
     {"P2M_NO_TVOTE": "1"},                     # chunk / batch votes by broadcast per group (not transposed)
     {"P2M_NO_TVOTE": "1", "P2M_SCAN_WARP": "1"},
     {"P2M_NO_SPATIAL": "1"},                   # lists scanned in ascending face order
