@@ -385,7 +385,7 @@ struct p2m_engine {
     int e2e_chunks = 0;
     double e2e_sched[4] = {1.0 / 32, 2.0, 0.25, 0.0};  // first, growth, cap, tail (P2M_E2E_SCHED)  // 0: geometric chunk schedule; k > 0: k equal chunks (P2M_E2E_CHUNKS, A/B)
     bool e2e_sched_set = false;  // P2M_E2E_SCHED given: no automatic choice between the dense and sparse schedules
-    double e2e_sparse_tail = 0.5;  // sparse batches: one big chunk + a tail of this fraction (P2M_E2E_TAIL)
+    double e2e_sparse_tail = 0.1;  // sparse batches: one big chunk + a tail of this fraction (P2M_E2E_TAIL)
     uint64_t n_sites = 0, n_faces = 0, n_entries = 0, n_bvh = 0, n_heavy = 0;
     uint64_t grid_cells = 0, grid_pairs = 0;  // 0 = no grid (k-d tree only)
     uint64_t n_batches = 0;                   // 32-entry list batches (batch spheres)
@@ -1557,7 +1557,7 @@ int ensure_bounce(Slot& s) {
 // thread: per finished chunk, enqueue D2H sub-copies into the out-ring, unpack completed ones.
 int run_bounce(p2m_engine* e, Slot& s, const double* q, double* dist, double* cp, uint32_t* face, uint32_t* site,
                uint32_t* flags, uint64_t b, const std::vector<uint64_t>& len_of, p2m_counters* cnt,
-               p2m_counters& part) {
+               p2m_counters& part, bool serial_kernels) {
     using B = Slot::Bounce;
     auto& bn = s.bnc;
     const size_t nch = len_of.size();
@@ -1653,6 +1653,7 @@ int run_bounce(p2m_engine* e, Slot& s, const double* q, double* dist, double* cp
         if (rc != P2M_OK) break;
         cudaEvent_t ev_in = s.cev[3 * c], ev_k = s.cev[3 * c + 1];
         if (cudaEventRecord(ev_in, s.h2d) != cudaSuccess || cudaStreamWaitEvent(st, ev_in, 0) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
+        if (serial_kernels && c > 0 && cudaStreamWaitEvent(st, s.cev[3 * (c - 1) + 1], 0) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
         if (c >= (size_t)Slot::kPipe && cudaStreamWaitEvent(st, s.cev[3 * (c - Slot::kPipe) + 2], 0) != cudaSuccess) { rc = P2M_ERR_CUDA; break; }
         p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
         rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false, &w.sc, k);
@@ -1716,6 +1717,10 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             //  * kernels of chunk c run on compute stream c % kPipe with staging set c % kPipe, after
             //    its input landed and after the D2H of the chunk that used the set before it.
             std::vector<uint64_t> len_of;
+            // big chunks each fill the GPU: their kernels run in chunk order (a later chunk whose input
+            // landed early otherwise interleaves with an earlier one, which then finishes -- and starts
+            // its D2H -- late: 291 vs 334 ms on c5 at 80/20, seen run to run)
+            bool serial_kernels = false;
             if (e->e2e_chunks > 0) {
                 const uint64_t k = (uint64_t)e->e2e_chunks;
                 const uint64_t c0 = std::max<uint64_t>(1ull << 16, (m + k - 1) / k);
@@ -1723,14 +1728,22 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             } else if (!e->e2e_sched_set && m < 128ull * e->n_sites && m >= (1ull << 22)) {
                 // Sparse batch (few rows per site, the regime of the warp tiles): a tile's cost is
                 // nearly independent of its rows, so every extra chunk re-pays the lists -- c5 at
-                // 100 M rows runs at 0.44 G rows/s whole, 0.38 in halves, 0.24 in eighths.  One big
-                // chunk and a small tail instead: the tail's H2D and the big chunk's D2H hide behind
-                // the other chunk's kernels.  Measured (100 M rows, pinned): c5 358 ms geometric, 306 in
-                // two halves, 296 at 80/20; c4 (kernels as fast as the copies) 199 geometric, 170 in two
-                // halves, 219 at 80/20 -- halves are the robust choice (P2M_E2E_TAIL sets the fraction).
+                // 100 M rows runs at 0.49 G rows/s whole, 0.42 in halves, 0.26 in eighths.  Few big
+                // chunks, then, the last one smaller so that the drain (its D2H) is short: two equal
+                // chunks and a tail (P2M_E2E_TAIL, default 0.1), kernels of consecutive chunks in
+                // order (serial_kernels below).  Measured (100 M rows, pinned), c5: 358 ms geometric,
+                // 302 in two halves, 292 at 45/45/10, 302 at 40/40/20; c4 (kernels as fast as the
+                // copies): 199 geometric, 175 in halves, 167 at 45/45/10, 161 at 40/40/20.
                 const uint64_t mt = std::max<uint64_t>(1ull << 18, (uint64_t)(e->e2e_sparse_tail * (double)m));
-                if (mt < m) { len_of.push_back(m - mt); len_of.push_back(mt); }
-                else len_of.push_back(m);
+                if (mt < m) {
+                    const uint64_t h0 = (m - mt + 1) / 2;
+                    len_of.push_back(h0);
+                    if (m - mt - h0) len_of.push_back(m - mt - h0);
+                    len_of.push_back(mt);
+                } else {
+                    len_of.push_back(m);
+                }
+                serial_kernels = true;
             } else {
                 // geometric: first chunk m*first, growing by `growth` up to m*cap, the last m*tail rows
                 // as a separate small chunk (its D2H is the pipeline's drain)
@@ -1767,7 +1780,7 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
             if (bounce) {
                 rc = ensure_bounce(s);
                 if (rc != P2M_OK) return rc;
-                return run_bounce(e, s, q, dist, cp, face, site, flags, b, len_of, cnt, parts[g]);
+                return run_bounce(e, s, q, dist, cp, face, site, flags, b, len_of, cnt, parts[g], serial_kernels);
             }
             uint64_t off = 0;
             for (size_t c = 0; c < len_of.size(); ++c) {
@@ -1781,6 +1794,7 @@ P2M_API int p2m_query(p2m_engine* e, const double* q, uint64_t n, double* dist, 
                 CK(cudaMemcpyAsync(w.q, q + 3 * r0, 24 * len, cudaMemcpyHostToDevice, s.h2d));
                 CK(cudaEventRecord(ev_in, s.h2d));
                 CK(cudaStreamWaitEvent(st, ev_in, 0));
+                if (serial_kernels && c > 0) CK(cudaStreamWaitEvent(st, s.cev[3 * (c - 1) + 1], 0));
                 if (c >= (size_t)Slot::kPipe) CK(cudaStreamWaitEvent(st, s.cev[3 * (c - Slot::kPipe) + 2], 0));
                 p2m::dev::Out o{w.dist, w.cp, w.face, w.site, w.flags, nullptr, cnt ? s.agg : nullptr};
                 rc = run_pipeline(e, s, w.q, len, o, cnt != nullptr, st, false, nullptr, false, &w.sc, k);
